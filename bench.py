@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Random-play env-steps/s benchmark (BASELINE.json metric) on 1..8 B200s.
+
+One "step" = one pass of the hot path over the whole batch: device random
+actions (agents.random_actions, agents.py:33-46) + the batched env step with
+auto-reset and fused observation emission (core.batch_step, core.py:353-386;
+the reference's bench_run loop, bench.py:121-129) + the episode counter.
+
+  python bench.py [--game go_19x19] [--batch 131072] [--steps K] [--warmup W]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (weak scaling: B per GPU)
+  python bench.py --impl reference ...                    (CPU reference arm)
+
+Rank 0 prints ONE JSON line. `value` = env-steps/s over all ranks with
+inputs resident in HBM; `e2e` = the same metric through the public
+batch_step API with host (pinned) action buffers and a per-step host read of
+rewards/terminated/truncated/current_player; `roofline` = the step kernel's
+algorithmic bytes per launch / its CUDA-event duration vs MEASURED_PEAKS.json.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic bytes per env-step (restated in DESIGN.md §4):
+# int64 action + float32 observation + bool mask + rewards/flags/player +
+# compact state read/write. The superko history scan is excluded.
+B_ALG = {"go_9x9": 5964, "go_19x19": 25860, "chess": 35502, "shogi": 41013, "backgammon": 400}
+DEFAULT_BATCH = {"go_9x9": 1 << 17, "go_19x19": 1 << 17, "chess": 1 << 17, "shogi": 1 << 16, "backgammon": 1 << 17}
+STEP_KERNEL = {"go_9x9": "go::step_kernel<9>", "go_19x19": "go::step_kernel<19>", "chess": "chess::step_kernel",
+               "shogi": "shogi::step_kernel", "backgammon": "bg::step_kernel"}
+METRIC = "random-play env steps/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--game", default="go_19x19")
+    ap.add_argument("--batch", type=int, default=0, help="envs per GPU (default per game, 2^17 for go_19x19)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="add a batch-size sweep 2^10..2^17 to the line")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bbk_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ GPU arm
+def run_gpu(args, rank, world, local):
+    import torch
+
+    import paper_2303_17503_b200 as bb
+    from paper_2303_17503_b200.core import resolve
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    game = args.game
+    gdef = resolve(game)
+    kern = gdef.batch_kernel
+    B = args.batch or DEFAULT_BATCH[game]
+    limit = gdef.max_steps
+    root = bb.RngKey(args.seed)
+    slot0 = rank * B   # global slot index: bit-identical to one big batch
+
+    # ping-pong device states: only the previous batch stays valid in bench mode
+    cur = kern.init(gdef, root.child(0), B, limit, slot0=slot0, device=dev)
+    spare = kern.new_v(B, slot0, dev, 0, limit)
+    acts = torch.empty(B, dtype=torch.int64, device=dev)
+    episodes = torch.zeros(1, dtype=torch.int64, device=dev)
+    lib = __import__("paper_2303_17503_b200._native", fromlist=["lib"]).lib()
+    stream = torch.cuda.current_stream(dev)
+    t = 0
+
+    def one_step(ev=None):
+        nonlocal cur, spare, t
+        kern.random_actions(cur, root.child(2 * t + 1), out=acts)
+        if ev is not None:
+            ev[0].record(stream)
+        nxt = kern.step(gdef, cur, acts, root.child(2 * (t + 1)), limit, validate=False, out=spare)
+        if ev is not None:
+            ev[1].record(stream)
+        lib.bbk_count_finished(nxt.dev.terminated.data_ptr(), nxt.dev.truncated.data_ptr(), B,
+                               episodes.data_ptr(), stream.cuda_stream)
+        spare, cur = cur, nxt
+        t += 1
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k in range(args.steps):
+        one_step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.all_reduce(episodes, op=dist.ReduceOp.SUM)
+        dist.barrier()
+    total_steps = B * world * args.steps
+    value = total_steps / (ms / 1e3)
+    avg_kern_ms = sum(kern_ms) / len(kern_ms)
+    peak, peak_kind = peaks()
+    achieved = B_ALG[game] * B / (avg_kern_ms / 1e3) / 1e9
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "env-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64/int8 (integer board logic; float32 observation output)",
+        "data": "synthetic: random-play rollouts from the reference key schedule (seed %d), auto-reset" % args.seed,
+        "config": {"workload": f"{game} random play with legal_action_mask + observation", "game": game,
+                   "batch_per_gpu": B, "global_batch": B * world, "max_steps": limit,
+                   "parallelism": f"dp{world} (independent env slices, global slot keys)",
+                   "l2": "per-step outputs exceed L2 (obs %.2f GB/step)" % (B * 4 * __import__("math").prod(
+                       gdef.spec.observation_shape) / 1e9),
+                   "timed": "K steps after W warm-up steps from init (step t of the BatchSession schedule)"},
+        "clocks": clk,
+        "gpu_launches": 3 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "kernel": STEP_KERNEL[game], "kernel_ms": avg_kern_ms,
+                     "kernel_share_of_step": avg_kern_ms / (ms / args.steps),
+                     "bytes_per_env_step": B_ALG[game]},
+        "episodes_completed": int(episodes.item()),
+    }
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, gdef, kern, cur, root, t, dev, world)
+    if args.sweep:
+        out["sweep"] = run_sweep(args, gdef, kern, dev, slot0)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, game, B, args.cpu_seconds)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return out
+
+
+def run_e2e(args, gdef, kern, cur, root, t, dev, world):
+    """Same metric through the public API with host buffers.
+
+    Per step: device random policy -> D2H of the actions into pinned host
+    memory (a host agent's output) -> core.batch_step(host actions) (H2D
+    inside) -> D2H of rewards/terminated/truncated/current_player, then the
+    host reads them (synchronous, as a host RL loop does).
+    """
+    import torch
+
+    from paper_2303_17503_b200.core import Batch, batch_step
+
+    B = cur.n
+    batch = Batch(gdef, B, gdef.max_steps, vstate=cur)
+    host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
+    host_r = torch.empty((B, 2), dtype=torch.float32, pin_memory=True)
+    host_f = torch.empty((B, 2), dtype=torch.uint8, pin_memory=True)
+    host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
+    steps = max(4, min(args.steps, 64))
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        a = kern.random_actions(batch._v, root.child(2 * t + 1))
+        host_act.copy_(a)
+        batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False)
+        d = batch.device
+        host_r.copy_(d.rewards, non_blocking=True)
+        host_f[:, 0].copy_(d.terminated, non_blocking=True)
+        host_f[:, 1].copy_(d.truncated, non_blocking=True)
+        host_cp.copy_(d.current_player, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        t += 1
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([dt], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    return {"value": B * world * steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
+            "d2h_bytes_per_step": (8 + 8 + 2 + 4) * B, "steps": steps,
+            "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player"}
+
+
+def run_sweep(args, gdef, kern, dev, slot0):
+    import torch
+
+    import paper_2303_17503_b200 as bb
+
+    res = {}
+    root = bb.RngKey(args.seed)
+    for e in range(10, 18):
+        B = 1 << e
+        if gdef.game_id == "shogi" and e > 16:
+            continue
+        cur = kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0, device=dev)
+        spare = kern.new_v(B, slot0, dev, 0, gdef.max_steps)
+        acts = torch.empty(B, dtype=torch.int64, device=dev)
+        n_steps = 64
+        t = 0
+        for k in range(8 + n_steps):
+            if k == 8:
+                torch.cuda.synchronize()
+                s, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+            kern.random_actions(cur, root.child(2 * t + 1), out=acts)
+            nxt = kern.step(gdef, cur, acts, root.child(2 * (t + 1)), gdef.max_steps, validate=False, out=spare)
+            spare, cur = cur, nxt
+            t += 1
+        e_.record()
+        torch.cuda.synchronize()
+        res[str(B)] = B * n_steps / (s.elapsed_time(e_) / 1e3)
+        del cur, spare
+    return {"env_steps_per_s": res, "steps": 64, "note": "steps 9..72 after init (early game)"}
+
+
+# ------------------------------------------------------------ CPU arms
+def cpu_run(game, n, seconds, threads):
+    """Oracle port (C, OpenMP) driven through the reference's bench loop, with observations."""
+    import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    sess = oracle.Session(game, n, 0)
+    # warm-up a few steps, then time whole steps until `seconds` elapse
+    for _ in range(3):
+        c = sess.b.columns(with_obs=True)
+        sess.step(sess.sample_random_actions(c))
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        c = sess.b.columns(with_obs=True)
+        sess.step(sess.sample_random_actions(c))
+        steps += 1
+        dt = time.perf_counter() - t0
+        if dt >= seconds:
+            break
+    return n * steps / dt, steps, dt
+
+
+def cpu_baseline(args, game, B, seconds):
+    threads = os.cpu_count() or 1
+    n = min(B, 512 if game in ("go_19x19", "chess", "shogi") else 4096)
+    v, steps, dt = cpu_run(game, n, seconds, threads)
+    return {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "port",
+            "sample": f"{game}: {n} envs x {steps} steps from init ({dt:.1f} s), oracle/orc_*.c (OpenMP) + "
+                      "numpy random_actions, observations emitted"}
+
+
+def run_reference(args, rank, world):
+    game = args.game
+    B = args.batch or DEFAULT_BATCH[game]
+    threads = os.cpu_count() or 1
+    n = min(B, 512 if game in ("go_19x19", "chess", "shogi") else 4096)
+    v, steps, dt = cpu_run(game, n, max(args.cpu_seconds, 5.0), threads)
+    return {
+        "metric": METRIC, "value": v, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int (CPU)", "data": "synthetic random play, seed %d" % args.seed,
+        "impl": "reference",
+        "config": {"workload": f"{game} random play with legal_action_mask + observation", "game": game,
+                   "batch_per_gpu": B},
+        "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} envs x {steps} steps ({dt:.1f} s); reference is pure Python "
+                                   "(no compilable C path), so the C restatement oracle/ is timed"},
+        "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        return 0
+    out = run_gpu(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,135 @@
+/* bbk.h -- C-ABI of the B200 batched board-game step (libbbk.so).
+ *
+ * This is the drop-in boundary for the reference's batch-kernel plugin
+ * protocol, `GameDef.batch_kernel` (reference pkg/src/boardbatch/core.py:88),
+ * whose three calls are
+ *     kern.init(gdef, key, n, limit)            core.py:346-348
+ *     kern.step(gdef, v, acts, key, limit)      core.py:366-368
+ *     kern.state_at(gdef, v, i, limit)          core.py:276-282
+ * (reference implementation: games/tictactoe.py:71-198). Every entry point
+ * below takes plain device pointers and sizes (no torch types), runs
+ * asynchronously on `stream` (a cudaStream_t, NULL = legacy default), and
+ * returns 0 or a cudaError_t. The host mirror of the protocol lives in
+ * paper_2303_17503_b200/games/*.py and binds these symbols with ctypes.
+ *
+ * Key contract (core.py:374, tictactoe.py:99-106): slot i uses
+ * k_i = child(key_state, slot0 + i) with child(k, j) = mix64(k + (j+1)*phi)
+ * (rng.py:43-45), or k_i = slot_keys[i] when slot_keys != NULL (the scalar
+ * init/step path, core.py:223-243). A reset draws the player permutation
+ * from child(k_i, 0) % 2 and the core from child(k_i, 1) (core.py:227-228).
+ *
+ * Layouts (row-major, batch leading, SURVEY §8a dtypes):
+ *   observation        float32 [n, *obs_shape]  current player's view
+ *   legal_action_mask  uint8   [n, A]           zero when finished
+ *   rewards            float32 [n, 2]           indexed by player
+ *   terminated, truncated uint8 [n]
+ *   current_player, step_count int32 [n]
+ *   player_to_role     int8    [n, 2]
+ */
+#ifndef BBK_H
+#define BBK_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBK_ABI_VERSION 1
+
+typedef struct bbk_cols {
+    float*    observation;        /* may be NULL: skip observation emission */
+    uint8_t*  legal_action_mask;
+    float*    rewards;
+    uint8_t*  terminated;
+    uint8_t*  truncated;
+    int32_t*  current_player;
+    int32_t*  step_count;
+    int8_t*   player_to_role;
+} bbk_cols;
+
+/* ------------------------------------------------------------------ Go --
+ * Replaces games/go.py (make_game(size), go.py:114-290): apply :219-262,
+ * legal_mask :121-174 (positional superko), score_rewards :176-210,
+ * observe :264-273, Core.encode :103-111.
+ *   pat[n, pat_stride]  uint16: bit 2t / 2t+1 = black / white stone at the
+ *                       point in boards_hist[t] (t = 0 newest .. 7)
+ *   history[n, hist_cap] uint64 append-only superko hashes (history set)
+ *   bloom[n, 256]        uint32 8192-bit Bloom filter over history
+ */
+#define BBK_GO_BLOOM_WORDS 256
+
+typedef struct bbk_go_state {
+    uint16_t* pat;
+    uint64_t* hash;
+    uint64_t* hist_xor;
+    int32_t*  hist_len;
+    uint8_t*  role_to_move;
+    uint8_t*  pass_count;
+} bbk_go_state;
+
+typedef struct bbk_go_store {
+    uint64_t* history;
+    uint32_t* bloom;
+    int32_t   hist_cap;
+} bbk_go_store;
+
+int bbk_go_pat_stride(int size);
+
+/* batch_init (core.py:340-350) */
+int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
+                int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                int32_t max_steps, void* stream);
+
+/* batch_step (core.py:353-386): auto-reset of finished slots, else go.apply.
+ * Actions are assumed legal (validate first with bbk_check_actions). */
+int bbk_go_step(int size, double komi, const bbk_cols* in, const bbk_go_state* in_s,
+                const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
+                const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state,
+                const uint64_t* slot_keys, int32_t max_steps, void* stream);
+
+/* observe(state, player) (core.py:246-251) for an explicit role per slot. */
+int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, void* stream);
+
+/* Rebuild Bloom filters from history[0:hist_len) (used when a batch branches). */
+int bbk_go_rebuild_bloom(const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream);
+
+/* ---------------------------------------------------------- Backgammon --
+ * Replaces games/backgammon.py: _legal_mask :62-95, _roll :125-130,
+ * _final :137-147, _apply :150-193, _observe :196-206, encode :113-119. */
+typedef struct bbk_bg_state {
+    int8_t*   points;     /* [n, 24] signed, + = role 0 */
+    uint8_t*  misc;       /* [n, 12]: bar0 bar1 off0 off1 role d1 d2 rem0..3 nrem */
+} bbk_bg_state;
+
+int bbk_bg_init(const bbk_cols* out, const bbk_bg_state* out_s, int64_t n, int64_t slot0,
+                uint64_t key_state, const uint64_t* slot_keys, int32_t max_steps, void* stream);
+int bbk_bg_step(const bbk_cols* in, const bbk_bg_state* in_s, const bbk_cols* out, const bbk_bg_state* out_s,
+                const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state,
+                const uint64_t* slot_keys, int32_t max_steps, void* stream);
+int bbk_bg_observe(const bbk_bg_state* s, const uint8_t* role, float* obs, int64_t n, void* stream);
+
+/* ------------------------------------------------------------- generic --
+ * agents.random_actions (agents.py:33-46): a_i = index of the d-th legal
+ * action, d = child(key, slot0+i) % max(popcount(mask_i), 1); 0 if none. */
+int bbk_random_actions(const uint8_t* mask, int64_t n, int32_t num_actions, uint64_t key_state,
+                       int64_t slot0, int64_t* actions, void* stream);
+
+/* IllegalAction check (core.py:234-239, tictactoe.py:111-121): writes the
+ * lowest live slot whose action is out of range or masked out into
+ * *first_bad (initialise it to INT32_MAX), finished slots are exempt. */
+int bbk_check_actions(const uint8_t* mask, const uint8_t* terminated, const uint8_t* truncated,
+                      const int64_t* actions, int64_t n, int32_t num_actions, int32_t* first_bad,
+                      void* stream);
+
+/* Sum of (terminated | truncated) over n slots, added into *count
+ * (bench.py:129 episode counter). */
+int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int64_t n,
+                       unsigned long long* count, void* stream);
+
+int bbk_abi_version(void);
+const char* bbk_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

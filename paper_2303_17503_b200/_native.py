@@ -1,0 +1,124 @@
+"""ctypes binding of the C-ABI in ``include/bbk.h`` (libbbk.so).
+
+There is no fallback: if the shared object is missing (and cannot be built
+because nvcc is absent) every engine call raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libbbk.so")
+
+_lock = threading.Lock()
+_lib = None
+
+
+class NativeUnavailable(RuntimeError):
+    """libbbk.so (the sm_100a kernels) is not built / not loadable."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a CUDA error code."""
+
+
+P = C.c_void_p
+I64 = C.c_int64
+U64 = C.c_uint64
+I32 = C.c_int32
+
+
+class Cols(C.Structure):
+    _fields_ = [("observation", P), ("legal_action_mask", P), ("rewards", P), ("terminated", P),
+                ("truncated", P), ("current_player", P), ("step_count", P), ("player_to_role", P)]
+
+
+class GoState(C.Structure):
+    _fields_ = [("pat", P), ("hash", P), ("hist_xor", P), ("hist_len", P), ("role_to_move", P),
+                ("pass_count", P)]
+
+
+class GoStore(C.Structure):
+    _fields_ = [("history", P), ("bloom", P), ("hist_cap", I32)]
+
+
+class BgState(C.Structure):
+    _fields_ = [("points", P), ("misc", P)]
+
+
+class ChessState(C.Structure):
+    _fields_ = [("board", P), ("misc", P), ("hist", P)]
+
+
+class ShogiState(C.Structure):
+    _fields_ = [("board", P), ("misc", P), ("hist", P)]
+
+
+def _declare(L):
+    ptr = C.POINTER
+    L.bbk_abi_version.restype = C.c_int
+    L.bbk_build_info.restype = C.c_char_p
+    L.bbk_go_pat_stride.argtypes = [C.c_int]
+    L.bbk_go_init.argtypes = [C.c_int, ptr(Cols), ptr(GoState), ptr(GoStore), I64, I64, U64, P, I32, P]
+    L.bbk_go_step.argtypes = [C.c_int, C.c_double, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
+                              P, I64, I64, U64, P, I32, P]
+    L.bbk_go_observe.argtypes = [C.c_int, P, P, P, I64, P]
+    L.bbk_go_rebuild_bloom.argtypes = [ptr(GoStore), P, I64, P]
+    L.bbk_bg_init.argtypes = [ptr(Cols), ptr(BgState), I64, I64, U64, P, I32, P]
+    L.bbk_bg_step.argtypes = [ptr(Cols), ptr(BgState), ptr(Cols), ptr(BgState), P, I64, I64, U64, P, I32, P]
+    L.bbk_bg_observe.argtypes = [ptr(BgState), P, P, I64, P]
+    L.bbk_random_actions.argtypes = [P, I64, I32, U64, I64, P, P]
+    L.bbk_check_actions.argtypes = [P, P, P, P, I64, I32, P, P]
+    L.bbk_count_finished.argtypes = [P, P, I64, P, P]
+    for g, S in (("chess", ChessState), ("shogi", ShogiState)):
+        if hasattr(L, f"bbk_{g}_step"):
+            getattr(L, f"bbk_{g}_init").argtypes = [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P]
+            getattr(L, f"bbk_{g}_step").argtypes = [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P]
+            getattr(L, f"bbk_{g}_observe").argtypes = [ptr(S), P, P, I64, P]
+    for name in dir(L):
+        pass
+    return L
+
+
+def lib():
+    """Load libbbk.so (building it in-tree first if sources are newer and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        from . import build as _build
+        try:
+            if _build.needs_build():
+                _build.build()
+        except Exception as exc:  # nvcc missing or compile error
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailable(f"libbbk.so is not built and could not be built: {exc}") from exc
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(f"{LIB_PATH} missing; run `python -m paper_2303_17503_b200.build`")
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as exc:
+            raise NativeUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
+        _lib = _declare(L)
+        return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what} failed with cudaError {rc}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream

@@ -1,0 +1,81 @@
+// Shared device helpers for the sm_100a board-game step kernels.
+//
+// RNG: bit-exact restatement of reference pkg/src/boardbatch/rng.py:22-45
+// (splitmix64 finaliser; child(k, i) = mix64(k + (i+1)*phi)). Keys are a pure
+// function of (root seed, step, GLOBAL slot index), so slicing a batch over
+// GPUs (slot0 offset) is bit-identical to one GPU.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define BBK_FULL 0xffffffffu
+
+namespace bbk {
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ULL;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t child(uint64_t s, uint64_t i) {
+    return mix64(s + (i + 1) * 0x9E3779B97F4A7C15ULL);
+}
+
+__device__ __forceinline__ uint64_t slot_key(const uint64_t* slot_keys, uint64_t key, int64_t slot0, int64_t i) {
+    return slot_keys ? slot_keys[i] : child(key, (uint64_t)(slot0 + i));
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+    uint32_t lo = __shfl_sync(BBK_FULL, (uint32_t)v, src);
+    uint32_t hi = __shfl_sync(BBK_FULL, (uint32_t)(v >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t warp_xor64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        uint32_t lo = __shfl_xor_sync(BBK_FULL, (uint32_t)v, o);
+        uint32_t hi = __shfl_xor_sync(BBK_FULL, (uint32_t)(v >> 32), o);
+        v ^= ((uint64_t)hi << 32) | lo;
+    }
+    return v;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(BBK_FULL, v, o);
+    return v;
+}
+
+// Write NBYTES bytes of a per-env record into a flat [n, NBYTES] byte stream.
+// `src` is shared memory laid out so that src[i] is record byte i - `off`
+// relative to a 16-byte aligned origin: callers stage bytes at
+// src_base + (dst_byte_offset & 15). Chunks fully inside the record use
+// 128-bit stores; the (at most two) partial edge chunks use byte stores, so
+// neighbouring records written by other warps are never touched.
+__device__ __forceinline__ void warp_emit_bytes(uint8_t* dst_stream, int64_t rec_start, int nbytes,
+                                                const uint8_t* staged /* 16B aligned, data at +off */) {
+    const int lane = lane_id();
+    const int64_t end = rec_start + nbytes;
+    const int64_t c0 = rec_start >> 4;            // first chunk (may be partial)
+    const int64_t c1 = (end + 15) >> 4;           // one past last chunk
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
+        const int64_t g0 = c << 4;
+        const uint8_t* s = staged + (g0 - (rec_start & ~(int64_t)15));
+        if (g0 >= rec_start && g0 + 16 <= end) {
+            *reinterpret_cast<uint4*>(dst_stream + g0) = *reinterpret_cast<const uint4*>(s);
+        } else {
+            for (int k = 0; k < 16; k++) {
+                int64_t g = g0 + k;
+                if (g >= rec_start && g < end) dst_stream[g] = s[k];
+            }
+        }
+    }
+}
+
+}  // namespace bbk

@@ -1,0 +1,637 @@
+// Go (Tromp-Taylor, positional superko) batched step for sm_100a.
+//
+// Replaces reference pkg/src/boardbatch/games/go.py for make_game(size)
+// (size 9 and 19 instantiated): apply :219-262, _analyse :45-80,
+// legal_mask :121-174, score_rewards :176-210, init_core :212-217,
+// observe :264-273, plus env-core _make_state core.py:192-220 and the
+// auto-reset of batch_step core.py:353-386.
+//
+// Mapping: one warp per board, lane r owns board row r as bit rows
+// (black, white, empty; bit c = column c). Per step:
+//   1. placement + captures: bit-parallel flood of each enemy neighbour
+//      group over the rows (shuffles), captured iff no liberty;
+//   2. analysis of the new board: union-find over horizontal RUNS (not
+//      cells) in shared memory, hooked with atomicCAS between vertically
+//      overlapping runs; per group "is in atari" from one atomicOr per run of
+//      OR(lib) | OR(~lib) (a group has exactly one liberty iff every
+//      liberty position is equal iff the two ORs are disjoint);
+//   3. legal mask: empty points with an empty neighbour / a non-atari own
+//      neighbour group / a capture (XOR of the captured atari groups'
+//      zobrist accumulated at their single liberty), filtered by positional
+//      superko through a per-env 8192-bit Bloom filter with an exact scan of
+//      the append-only history on a Bloom hit (identical answers to the
+//      reference's `h2 not in history`);
+//   4. observation: the 8-deep board history is kept TRANSPOSED per point
+//      (uint16 `pat`, bit 2t/2t+1 = black/white in boards_hist[t]), so the
+//      17 planes of a point are one shift/swap of pat plus the colour bit;
+//      the [N,N,17] float32 record is emitted as a flat 16-byte-aligned
+//      stream with 128-bit stores (records are not 16-B aligned).
+#include <cstdio>
+#include "common.cuh"
+#include "../../include/bbk.h"
+
+namespace go {
+using namespace bbk;
+
+constexpr int kWarps = 4;             // warps (boards in flight) per CTA
+constexpr int kPlanes = 17;
+constexpr int kBloomBits = BBK_GO_BLOOM_WORDS * 32;   // 8192
+
+__host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
+
+template <int N>
+struct WarpSmem {
+    static constexpr int C = N * N;
+    static constexpr int A = C + 1;
+    uint32_t bloom[BBK_GO_BLOOM_WORDS];
+    uint64_t capx[C];
+    uint32_t par[C];
+    uint32_t gst[C];
+    uint32_t P[C + 4];
+    alignas(16) uint16_t pat[pat_stride(N)];
+    alignas(16) uint8_t mb[((A + 47) & ~15)];
+    uint32_t capbits[32];
+    uint32_t rowB[32];
+    uint32_t rowW[32];
+    uint64_t hit[32];
+};
+
+template <int N>
+struct BlockSmem {
+    static constexpr int C = N * N;
+    uint64_t zob[2 * C];     // [0,C) black, [C,2C) white  (go.py:20-25)
+    float4 lut[16];
+    WarpSmem<N> w[kWarps];
+};
+
+struct StepParams {
+    bbk_cols in, out;
+    bbk_go_state in_s, out_s;
+    bbk_go_store store;
+    const int64_t* actions;
+    const uint64_t* slot_keys;
+    int64_t n, slot0;
+    uint64_t key;
+    int32_t max_steps;
+    double komi;
+    int force_reset;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t run_at(uint32_t X, int s) {
+    uint32_t len = __ffs(~(X >> s)) - 1;
+    return ((1u << len) - 1u) << s;
+}
+
+__device__ __forceinline__ uint32_t uf_find(volatile uint32_t* par, uint32_t x) {
+    uint32_t p;
+    while ((p = par[x]) != x) x = p;
+    return x;
+}
+
+__device__ __forceinline__ void uf_union(uint32_t* par, uint32_t a, uint32_t b) {
+    volatile uint32_t* vp = par;
+    while (true) {
+        a = uf_find(vp, a);
+        b = uf_find(vp, b);
+        if (a == b) return;
+        if (a < b) { uint32_t t = a; a = b; b = t; }
+        uint32_t old = atomicCAS(&par[a], a, b);
+        if (old == a) return;
+    }
+}
+
+__device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
+    uint32_t i1 = (uint32_t)h & (kBloomBits - 1);
+    uint32_t i2 = (uint32_t)(h >> 13) & (kBloomBits - 1);
+    uint32_t i3 = (uint32_t)(h >> 26) & (kBloomBits - 1);
+    return ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & (bloom[i3 >> 5] >> (i3 & 31)) & 1u) != 0;
+}
+
+// Lane 0 only: add h to both the shared copy and the env's global filter.
+__device__ __forceinline__ void bloom_add(uint32_t* sb, uint32_t* gb, uint64_t h) {
+    uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
+                       (uint32_t)(h >> 26) & (kBloomBits - 1)};
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        uint32_t w = idx[j] >> 5;
+        sb[w] |= 1u << (idx[j] & 31);
+        if (gb) gb[w] = sb[w];
+    }
+}
+
+__device__ __forceinline__ uint32_t up_row(uint32_t v, int lane) {
+    uint32_t u = __shfl_up_sync(BBK_FULL, v, 1);
+    return lane > 0 ? u : 0u;
+}
+__device__ __forceinline__ uint32_t dn_row(uint32_t v, int lane) {
+    uint32_t d = __shfl_down_sync(BBK_FULL, v, 1);
+    return lane < 31 ? d : 0u;
+}
+template <int N>
+__device__ __forceinline__ uint32_t dilate(uint32_t F, int lane) {
+    constexpr uint32_t ROW = (1u << N) - 1u;
+    return ((F << 1) | (F >> 1) | up_row(F, lane) | dn_row(F, lane)) & ROW;
+}
+
+// Tromp-Taylor area score (go.py:176-210), bit-parallel: an empty region
+// borders colour X iff it is reachable through empties from a point adjacent
+// to X. Returns role rewards (black, white).
+template <int N>
+__device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0, float& r1) {
+    constexpr uint32_t ROW = (1u << N) - 1u;
+    const uint32_t rowm = lane < N ? ROW : 0u;
+    uint32_t E = ~(Bk | Wh) & rowm;
+    uint32_t RB = dilate<N>(Bk, lane) & E, RW = dilate<N>(Wh, lane) & E;
+    while (true) {
+        uint32_t nb = (RB | dilate<N>(RB, lane)) & E;
+        uint32_t nw = (RW | dilate<N>(RW, lane)) & E;
+        bool ch = __any_sync(BBK_FULL, (nb != RB) || (nw != RW));
+        RB = nb; RW = nw;
+        if (!ch) break;
+    }
+    int black = warp_sum(__popc(Bk) + __popc(E & RB & ~RW));
+    int white = warp_sum(__popc(Wh) + __popc(E & RW & ~RB));
+    double b = black, w = white + komi;
+    if (b > w) { r0 = 1.0f; r1 = -1.0f; }
+    else if (w > b) { r0 = -1.0f; r1 = 1.0f; }
+    else { r0 = 0.0f; r1 = 0.0f; }
+}
+
+// Legal mask rows for the side to move (go.py:121-174, allow_self_capture
+// off). X = mover's stones, Y = opponent's stones, E = empties (row bits of
+// this lane). `zX`/`zY` are the zobrist tables of the two colours.
+template <int N>
+__device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_t* zY, uint32_t X, uint32_t Y,
+                               uint32_t E, uint64_t h, const uint64_t* hist, int nscan, uint64_t extra, int lane) {
+    constexpr uint32_t ROW = (1u << N) - 1u;
+    const int r = lane;
+    const uint32_t SX = X & ~(X << 1), SY = Y & ~(Y << 1);
+    // 1. run starts are union-find nodes
+    for (uint32_t s_ = SX | SY; s_; s_ &= s_ - 1) {
+        uint32_t node = r * N + (__ffs(s_) - 1);
+        S.par[node] = node;
+        S.gst[node] = 0u;
+    }
+    S.capbits[lane] = 0u;
+    __syncwarp();
+    // 2. hook each run to the vertically overlapping runs of the row above
+    {
+        const uint32_t Xu = up_row(X, lane), Yu = up_row(Y, lane);
+        const uint32_t SXu = Xu & ~(Xu << 1), SYu = Yu & ~(Yu << 1);
+#pragma unroll
+        for (int col = 0; col < 2; col++) {
+            const uint32_t Z = col ? Y : X, Zu = col ? Yu : Xu, SZ = col ? SY : SX, SZu = col ? SYu : SXu;
+            for (uint32_t s_ = SZ; s_; s_ &= s_ - 1) {
+                int s = __ffs(s_) - 1;
+                uint32_t V = run_at(Z, s) & Zu;
+                while (V) {
+                    int c = __ffs(V) - 1;
+                    int st = 31 - __clz(SZu & ((2u << c) - 1u));
+                    V &= ~run_at(Zu, st);
+                    uf_union(S.par, r * N + s, (r - 1) * N + st);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // 3. liberty position OR-stats per group root
+    const uint32_t Eu = up_row(E, lane), Ed = dn_row(E, lane);
+    for (uint32_t s_ = SX | SY; s_; s_ &= s_ - 1) {
+        int s = __ffs(s_) - 1;
+        uint32_t run = run_at((SX >> s) & 1 ? X : Y, s);
+        uint32_t up = run & Eu, dn = run & Ed, sd = ((run << 1) | (run >> 1)) & E;
+        if (!(up | dn | sd)) continue;
+        uint32_t lo = up ? (r - 1) * N + __ffs(up) - 1 : sd ? r * N + __ffs(sd) - 1 : (r + 1) * N + __ffs(dn) - 1;
+        uint32_t hi = dn ? (r + 1) * N + 31 - __clz(dn) : sd ? r * N + 31 - __clz(sd) : (r - 1) * N + 31 - __clz(up);
+        uint32_t root = uf_find(S.par, r * N + s);
+        atomicOr(&S.gst[root], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
+    }
+    __syncwarp();
+    // 4. atari classification. NA: mover stones whose group has >= 2 libs.
+    uint32_t NA = 0u, atY = 0u;
+    for (uint32_t s_ = SX; s_; s_ &= s_ - 1) {
+        int s = __ffs(s_) - 1;
+        uint32_t g = S.gst[uf_find(S.par, r * N + s)];
+        if ((g & (g >> 10) & 0x3FFu) != 0u) NA |= run_at(X, s);
+    }
+    for (uint32_t s_ = SY; s_; s_ &= s_ - 1) {
+        int s = __ffs(s_) - 1;
+        uint32_t g = S.gst[uf_find(S.par, r * N + s)];
+        if ((g & 0x80000000u) && (g & (g >> 10) & 0x3FFu) == 0u) {
+            uint32_t lib = g & 0x3FFu;
+            atY |= 1u << s;
+            S.capx[lib] = 0ull;
+            atomicOr(&S.capbits[lib / N], 1u << (lib % N));
+        }
+    }
+    __syncwarp();
+    for (uint32_t s_ = atY; s_; s_ &= s_ - 1) {
+        int s = __ffs(s_) - 1;
+        uint32_t lib = S.gst[uf_find(S.par, r * N + s)] & 0x3FFu;
+        uint64_t x = 0ull;
+        for (uint32_t b = run_at(Y, s); b; b &= b - 1) x ^= zY[r * N + __ffs(b) - 1];
+        atomicXor(reinterpret_cast<unsigned long long*>(&S.capx[lib]), (unsigned long long)x);
+    }
+    __syncwarp();
+    // 5. candidates + superko filter
+    const uint32_t capb = lane < N ? S.capbits[lane] : 0u;
+    const uint32_t NAu = up_row(NA, lane), NAd = dn_row(NA, lane);
+    const uint32_t nb = ((E << 1) | (E >> 1) | Eu | Ed | (NA << 1) | (NA >> 1) | NAu | NAd) & ROW;
+    const uint32_t cand = E & (capb | nb);
+    uint32_t legal = 0u, pend = 0u;
+    for (uint32_t c_ = cand; c_; c_ &= c_ - 1) {
+        int p = __ffs(c_) - 1;
+        int cell = r * N + p;
+        uint64_t h2 = h ^ zX[cell];
+        if ((capb >> p) & 1u) h2 ^= S.capx[cell];
+        if (bloom_maybe(S.bloom, h2)) pend |= 1u << p;
+        else legal |= 1u << p;
+    }
+    while (__any_sync(BBK_FULL, pend != 0u)) {
+        const unsigned active = __ballot_sync(BBK_FULL, pend != 0u);
+        int p = pend ? __ffs(pend) - 1 : 0;
+        uint64_t h2 = 0ull;
+        if (pend) {
+            int cell = r * N + p;
+            h2 = h ^ zX[cell];
+            if ((capb >> p) & 1u) h2 ^= S.capx[cell];
+            S.hit[lane] = h2;
+        }
+        __syncwarp();
+        unsigned found = 0u;
+        for (int j = lane; j < nscan + 1; j += 32) {
+            uint64_t v = j < nscan ? hist[j] : extra;
+            for (unsigned a_ = active; a_; a_ &= a_ - 1) {
+                int l = __ffs(a_) - 1;
+                if (v == S.hit[l]) found |= 1u << l;
+            }
+        }
+        found = __reduce_or_sync(BBK_FULL, found);
+        if (pend) {
+            if (!((found >> lane) & 1u)) legal |= 1u << p;
+            pend &= pend - 1u;
+        }
+        __syncwarp();
+    }
+    return legal;
+}
+
+// Observation of one board from the transposed history in S.pat (new
+// state), colour plane = role (go.py:264-273). Flat-stream emission.
+template <int N>
+__device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t b, int role, int lane) {
+    constexpr int C = N * N;
+    constexpr int NF = C * kPlanes;
+    for (int i = lane; i < C; i += 32) {
+        uint32_t v = S.pat[i];
+        if (role) v = ((v & 0x5555u) << 1) | ((v >> 1) & 0x5555u);
+        S.P[i] = v | ((uint32_t)role << 16);
+    }
+    if (lane < 4) S.P[C + lane] = 0u;
+    __syncwarp();
+    const int64_t F0 = b * (int64_t)NF;
+    const int64_t a0 = (F0 + 3) & ~(int64_t)3, a1 = (F0 + NF) & ~(int64_t)3;
+    if (lane < 8) {   // scalar head (<=3 floats) and tail (<=3 floats)
+        int64_t f = lane < 4 ? F0 + lane : a1 + (lane - 4);
+        bool ok = lane < 4 ? f < a0 : f < F0 + NF;
+        if (ok) {
+            uint32_t fi = (uint32_t)(f - F0);
+            uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;
+            obs[f] = (float)((S.P[c] >> k) & 1u);
+        }
+    }
+    float4* o4 = reinterpret_cast<float4*>(obs);
+    for (int64_t j = (a0 >> 2) + lane; j < (a1 >> 2); j += 32) {
+        uint32_t fi = (uint32_t)((j << 2) - F0);
+        uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;   // fi/17, exact for fi < 65536
+        uint64_t w = (uint64_t)S.P[c] | ((uint64_t)S.P[c + 1] << 17);
+        o4[j] = lut[(uint32_t)(w >> k) & 15u];
+    }
+    __syncwarp();
+}
+
+template <int N>
+__device__ __forceinline__ void init_block(BlockSmem<N>& B) {
+    constexpr int C = N * N;
+    const uint64_t base = 0x60D00D60C0FFEE00ULL + (uint64_t)N;   // go.py:22
+    for (int i = threadIdx.x; i < 2 * C; i += blockDim.x) {
+        int cell = i < C ? i : i - C, colour = i < C ? 0 : 1;
+        B.zob[i] = mix64(base + 2ull * (uint64_t)cell + (uint64_t)colour);
+    }
+    if (threadIdx.x < 16) {
+        uint32_t n = threadIdx.x;
+        B.lut[n] = make_float4((float)(n & 1), (float)((n >> 1) & 1), (float)((n >> 2) & 1), (float)((n >> 3) & 1));
+    }
+    __syncthreads();
+}
+
+template <int N>
+__global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
+    constexpr int C = N * N;
+    constexpr int A = C + 1;
+    constexpr int PS = pat_stride(N);
+    constexpr uint32_t ROW = (1u << N) - 1u;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BlockSmem<N>& B = *reinterpret_cast<BlockSmem<N>*>(smem_raw);
+    init_block<N>(B);
+    const int lane = lane_id();
+    WarpSmem<N>& S = B.w[threadIdx.x >> 5];
+    const uint32_t rowm = lane < N ? ROW : 0u;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
+        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+        const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
+        uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
+        uint32_t* gbloom = p.store.bloom + b * (int64_t)BBK_GO_BLOOM_WORDS;
+        int8_t p2r0, p2r1;
+        int role, pass_count, step, hlen;
+        uint64_t h, hx;
+        uint32_t Bk = 0u, Wh = 0u;
+        bool terminal = false;
+        float rr0 = 0.0f, rr1 = 0.0f;
+        int nscan;
+        uint64_t extra;
+        if (reset) {
+            // init (core.py:223-229) + init_core (go.py:212-217)
+            int c = (int)(child(k, 0) % 2ull);
+            p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
+            role = 0; pass_count = 0; step = 0; h = 0ull; hx = 0ull; hlen = 1;
+            for (int i = lane; i < PS; i += 32) S.pat[i] = 0;
+            for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) S.bloom[i] = 0u;
+            __syncwarp();
+            if (lane == 0) { bloom_add(S.bloom, nullptr, 0ull); hist[0] = 0ull; }
+            __syncwarp();
+            for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) gbloom[i] = S.bloom[i];
+            nscan = 0; extra = 0ull;
+        } else {
+            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
+            role = p.in_s.role_to_move[b]; pass_count = p.in_s.pass_count[b];
+            step = p.in.step_count[b];
+            h = p.in_s.hash[b]; hx = p.in_s.hist_xor[b]; hlen = p.in_s.hist_len[b];
+            const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
+            for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+            const uint4* gb4 = reinterpret_cast<const uint4*>(gbloom);
+            for (int i = lane; i < BBK_GO_BLOOM_WORDS / 4; i += 32) reinterpret_cast<uint4*>(S.bloom)[i] = gb4[i];
+            __syncwarp();
+            if (lane < N) {
+#pragma unroll 4
+                for (int col = 0; col < N; col++) {
+                    uint32_t v = S.pat[lane * N + col];
+                    Bk |= (v & 1u) << col;
+                    Wh |= ((v >> 1) & 1u) << col;
+                }
+            }
+            const int a = (int)p.actions[b];
+            step += 1;
+            nscan = hlen; extra = h;
+            if (a < 0 || a >= C) {   // pass (go.py:222-230)
+                pass_count += 1;
+                if (pass_count == 2) {
+                    terminal = true;
+                    score<N>(Bk, Wh, p.komi, lane, rr0, rr1);
+                }
+            } else {                 // placement (go.py:232-262)
+                const int ra = a / N, ca = a - ra * N;
+                uint32_t M = role == 0 ? Bk : Wh, O = role == 0 ? Wh : Bk;
+                if (lane == ra) M |= 1u << ca;
+                const uint32_t E0 = ~(M | O) & rowm;
+                const uint64_t* zM = B.zob + role * C;
+                const uint64_t* zO = B.zob + (1 - role) * C;
+                uint64_t capxor = 0ull;
+                uint32_t visited = 0u, dead = 0u;
+                const int qr_[4] = {ra - 1, ra + 1, ra, ra};
+                const int qc_[4] = {ca, ca, ca - 1, ca + 1};
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int qr = qr_[j], qc = qc_[j];
+                    if (qr < 0 || qr >= N || qc < 0 || qc >= N) continue;
+                    const uint32_t Oq = __shfl_sync(BBK_FULL, O, qr);
+                    const uint32_t Vq = __shfl_sync(BBK_FULL, visited, qr);
+                    if (!((Oq >> qc) & 1u) || ((Vq >> qc) & 1u)) continue;
+                    // quick exit: the stone itself touches an empty point
+                    const uint32_t Er = __shfl_sync(BBK_FULL, E0, qr);
+                    const uint32_t Eup = qr > 0 ? __shfl_sync(BBK_FULL, E0, qr - 1) : 0u;
+                    const uint32_t Edn = qr < N - 1 ? __shfl_sync(BBK_FULL, E0, qr + 1) : 0u;
+                    if ((((Er << 1) | (Er >> 1) | Eup | Edn) >> qc) & 1u) continue;
+                    uint32_t F = lane == qr ? (1u << qc) : 0u;
+                    while (true) {
+                        uint32_t F2 = (F | dilate<N>(F, lane)) & O;
+                        bool ch = __any_sync(BBK_FULL, F2 != F);
+                        F = F2;
+                        if (!ch) break;
+                    }
+                    visited |= F;
+                    if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E0) != 0u)) dead |= F;
+                }
+                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zO[lane * N + __ffs(d_) - 1];
+                O &= ~dead;
+                const uint64_t h2 = h ^ zM[a] ^ warp_xor64(capxor);
+                if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
+                if (lane == 0) {
+                    hist[hlen] = h2;
+                    bloom_add(S.bloom, gbloom, h2);
+                }
+                nscan = hlen; extra = h2;
+                hlen += 1; h = h2; hx ^= h2; pass_count = 0;
+            }
+            role = 1 - role;
+        }
+        // new transposed history: pat' = pat << 2 | current board (go.py:224, 260)
+        if (lane < 32) { S.rowB[lane] = Bk; S.rowW[lane] = Wh; }
+        __syncwarp();
+        uint16_t* opat = p.out_s.pat + b * (int64_t)PS;
+        if (!reset) {
+            for (int i = lane; i < C; i += 32) {
+                int rr = i / N, cc = i - rr * N;
+                uint32_t v = ((uint32_t)S.pat[i] << 2) | ((S.rowB[rr] >> cc) & 1u) | (((S.rowW[rr] >> cc) & 1u) << 1);
+                S.pat[i] = (uint16_t)v;
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < PS / 8; i += 32)
+            reinterpret_cast<uint4*>(opat)[i] = reinterpret_cast<const uint4*>(S.pat)[i];
+        const bool truncated = !terminal && step >= p.max_steps;
+        // legal mask of the new mover (skipped once the slot is finished)
+        uint32_t legal = 0u;
+        if (!terminal && !truncated) {
+            const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
+            const uint32_t E = ~(Bk | Wh) & rowm;
+            legal = legal_rows<N>(S, B.zob + role * C, B.zob + (1 - role) * C, X, Y, E, h, hist, nscan, extra, lane);
+        }
+        // stage mask bytes at the destination's 16-byte phase and emit
+        const int64_t mstart = b * (int64_t)A;
+        const int moff = (int)(mstart & 15);
+        if (lane < N) {
+            for (int col = 0; col < N; col++) S.mb[moff + lane * N + col] = (uint8_t)((legal >> col) & 1u);
+        }
+        if (lane == 0) S.mb[moff + C] = (uint8_t)(!terminal && !truncated);
+        __syncwarp();
+        warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.mb);
+        if (p.out.observation) emit_obs<N>(S, B.lut, p.out.observation, b, role, lane);
+        if (lane == 0) {
+            float r0 = 0.0f, r1 = 0.0f;
+            if (!truncated && (rr0 != 0.0f || rr1 != 0.0f)) {   // core.py:197-204
+                r0 = p2r0 == 0 ? rr0 : rr1;
+                r1 = p2r1 == 0 ? rr0 : rr1;
+            }
+            p.out.rewards[2 * b] = r0;
+            p.out.rewards[2 * b + 1] = r1;
+            p.out.terminated[b] = terminal;
+            p.out.truncated[b] = truncated;
+            p.out.step_count[b] = step;
+            p.out.current_player[b] = p2r0 == role ? 0 : 1;   // perm.index(role_to_move)
+            p.out.player_to_role[2 * b] = p2r0;
+            p.out.player_to_role[2 * b + 1] = p2r1;
+            p.out_s.hash[b] = h;
+            p.out_s.hist_xor[b] = hx;
+            p.out_s.hist_len[b] = hlen;
+            p.out_s.role_to_move[b] = (uint8_t)role;
+            p.out_s.pass_count[b] = (uint8_t)pass_count;
+        }
+        __syncwarp();
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kWarps * 32) observe_kernel(const uint16_t* pat, const uint8_t* role, float* obs, int64_t n) {
+    constexpr int PS = pat_stride(N);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BlockSmem<N>& B = *reinterpret_cast<BlockSmem<N>*>(smem_raw);
+    if (threadIdx.x < 16) {
+        uint32_t q = threadIdx.x;
+        B.lut[q] = make_float4((float)(q & 1), (float)((q >> 1) & 1), (float)((q >> 2) & 1), (float)((q >> 3) & 1));
+    }
+    __syncthreads();
+    const int lane = lane_id();
+    WarpSmem<N>& S = B.w[threadIdx.x >> 5];
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < n; b += nwarps) {
+        const uint4* src = reinterpret_cast<const uint4*>(pat + b * (int64_t)PS);
+        for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+        __syncwarp();
+        emit_obs<N>(S, B.lut, obs, b, role[b], lane);
+    }
+}
+
+__global__ void rebuild_bloom_kernel(bbk_go_store st, const int32_t* hist_len, int64_t n) {
+    __shared__ uint32_t sb[kWarps][BBK_GO_BLOOM_WORDS];
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + w; b < n; b += nwarps) {
+        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) sb[w][i] = 0u;
+        __syncwarp();
+        const uint64_t* hist = st.history + b * (int64_t)st.hist_cap;
+        for (int j = lane; j < hist_len[b]; j += 32) {
+            uint64_t h = hist[j];
+            uint32_t i1 = (uint32_t)h & (kBloomBits - 1), i2 = (uint32_t)(h >> 13) & (kBloomBits - 1),
+                     i3 = (uint32_t)(h >> 26) & (kBloomBits - 1);
+            atomicOr(&sb[w][i1 >> 5], 1u << (i1 & 31));
+            atomicOr(&sb[w][i2 >> 5], 1u << (i2 & 31));
+            atomicOr(&sb[w][i3 >> 5], 1u << (i3 & 31));
+        }
+        __syncwarp();
+        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) st.bloom[b * BBK_GO_BLOOM_WORDS + i] = sb[w][i];
+        __syncwarp();
+    }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <int N>
+static int launch_step(const StepParams& p, cudaStream_t stream) {
+    const size_t smem = sizeof(BlockSmem<N>);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(step_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<N>, kWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t need = (p.n + kWarps - 1) / kWarps;
+    int64_t grid = (int64_t)num_sms() * per_sm;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+template <int N>
+static int launch_observe(const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, cudaStream_t stream) {
+    const size_t smem = sizeof(BlockSmem<N>);
+    cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t need = (n + kWarps - 1) / kWarps;
+    int64_t grid = need < (int64_t)num_sms() * 4 ? need : (int64_t)num_sms() * 4;
+    observe_kernel<N><<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, smem, stream>>>(pat, role, obs, n);
+    return (int)cudaGetLastError();
+}
+
+static int dispatch_step(int size, const StepParams& p, cudaStream_t s) {
+    switch (size) {
+        case 9: return launch_step<9>(p, s);
+        case 13: return launch_step<13>(p, s);
+        case 19: return launch_step<19>(p, s);
+        default: return (int)cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace go
+
+extern "C" {
+
+int bbk_go_pat_stride(int size) { return go::pat_stride(size); }
+
+int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
+                int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    go::StepParams p{};
+    p.out = *out; p.out_s = *out_s; p.store = *store;
+    p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.komi = 0.0; p.force_reset = 1;
+    return go::dispatch_step(size, p, (cudaStream_t)stream);
+}
+
+int bbk_go_step(int size, double komi, const bbk_cols* in, const bbk_go_state* in_s,
+                const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
+                const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state,
+                const uint64_t* slot_keys, int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    go::StepParams p{};
+    p.in = *in; p.in_s = *in_s; p.out = *out; p.out_s = *out_s; p.store = *store;
+    p.actions = actions; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.komi = komi; p.force_reset = 0;
+    return go::dispatch_step(size, p, (cudaStream_t)stream);
+}
+
+int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, void* stream) {
+    if (n <= 0) return 0;
+    switch (size) {
+        case 9: return go::launch_observe<9>(pat, role, obs, n, (cudaStream_t)stream);
+        case 13: return go::launch_observe<13>(pat, role, obs, n, (cudaStream_t)stream);
+        case 19: return go::launch_observe<19>(pat, role, obs, n, (cudaStream_t)stream);
+        default: return (int)cudaErrorInvalidValue;
+    }
+}
+
+int bbk_go_rebuild_bloom(const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream) {
+    if (n <= 0) return 0;
+    int64_t grid = (n + go::kWarps - 1) / go::kWarps;
+    if (grid > 148 * 8) grid = 148 * 8;
+    go::rebuild_bloom_kernel<<<(unsigned)grid, go::kWarps * 32, 0, (cudaStream_t)stream>>>(*store, hist_len, n);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

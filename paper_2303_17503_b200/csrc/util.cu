@@ -1,0 +1,136 @@
+// Generic per-slot kernels shared by every game.
+//   bbk_random_actions  -- agents.random_actions (reference agents.py:33-46)
+//   bbk_check_actions   -- IllegalAction detection (core.py:234-239, tictactoe.py:111-121)
+//   bbk_count_finished  -- episode counter of bench_run (bench.py:129)
+#include "common.cuh"
+#include "../../include/bbk.h"
+
+namespace util {
+using namespace bbk;
+
+// Byte j of a mask row packed as 0/1 per byte; returns the word's flags
+// restricted to bytes in [lo, hi) of the row (row byte = 4*w + k - head).
+__device__ __forceinline__ uint32_t row_word(const uint8_t* mask, int64_t rs, int A, int w) {
+    // covered row bytes: [4w - head, 4w - head + 4)
+    const int64_t g0 = ((rs & ~(int64_t)3)) + 4 * (int64_t)w;   // global byte of this word
+    if (g0 >= rs && g0 + 4 <= rs + A) return *reinterpret_cast<const uint32_t*>(mask + g0) & 0x01010101u;
+    uint32_t v = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        int64_t g = g0 + k;
+        if (g >= rs && g < rs + A) v |= (uint32_t)(mask[g] & 1u) << (8 * k);
+    }
+    return v;
+}
+
+__global__ void random_actions_kernel(const uint8_t* mask, int64_t n, int A, uint64_t key, int64_t slot0,
+                                      int64_t* out) {
+    const int lane = lane_id();
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < n; b += nwarps) {
+        const int64_t rs = b * (int64_t)A;
+        const int head = (int)(rs & 3);
+        const int nwords = (head + A + 3) >> 2;
+        int cnt = 0;
+        for (int w = lane; w < nwords; w += 32) cnt += __popc(row_word(mask, rs, A, w));
+        const int total = warp_sum(cnt);
+        const uint64_t d64 = child(key, (uint64_t)(slot0 + b)) % (uint64_t)(total > 0 ? total : 1);
+        const int d = (int)d64;
+        int64_t action = 0;
+        if (total > 0) {
+            int base = 0;
+            for (int w0 = 0; w0 < nwords; w0 += 32) {
+                const int w = w0 + lane;
+                const uint32_t v = w < nwords ? row_word(mask, rs, A, w) : 0u;
+                const int c = __popc(v);
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int t = __shfl_up_sync(BBK_FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const int tot = __shfl_sync(BBK_FULL, incl, 31);
+                if (base + tot > d) {
+                    const int excl = base + incl - c;
+                    const bool mine = d >= excl && d < base + incl;
+                    int pos = 0;
+                    if (mine) {
+                        uint32_t x = v;
+                        for (int r = d - excl; r > 0; r--) x &= x - 1;
+                        pos = 4 * w + ((__ffs(x) - 1) >> 3) - head;
+                    }
+                    const unsigned who = __ballot_sync(BBK_FULL, mine);
+                    action = __shfl_sync(BBK_FULL, pos, __ffs(who) - 1);
+                    break;
+                }
+                base += tot;
+            }
+        }
+        if (lane == 0) out[b] = action;
+    }
+}
+
+__global__ void check_actions_kernel(const uint8_t* mask, const uint8_t* term, const uint8_t* trunc,
+                                     const int64_t* actions, int64_t n, int A, int32_t* first_bad) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    if (term[b] || trunc[b]) return;
+    int64_t a = actions[b];
+    bool bad = a < 0 || a >= A || !mask[b * (int64_t)A + a];
+    if (bad) atomicMin(first_bad, (int32_t)b);
+}
+
+__global__ void count_finished_kernel(const uint8_t* term, const uint8_t* trunc, int64_t n,
+                                      unsigned long long* count) {
+    int c = 0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x)
+        c += (term[b] | trunc[b]) ? 1 : 0;
+    c = warp_sum(c);
+    __shared__ int part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0 && v) atomicAdd(count, (unsigned long long)v);
+    }
+}
+
+}  // namespace util
+
+extern "C" {
+
+int bbk_random_actions(const uint8_t* mask, int64_t n, int32_t num_actions, uint64_t key_state,
+                       int64_t slot0, int64_t* actions, void* stream) {
+    if (n <= 0) return 0;
+    int64_t blocks = (n + 7) / 8;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    util::random_actions_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(mask, n, num_actions, key_state,
+                                                                                  slot0, actions);
+    return (int)cudaGetLastError();
+}
+
+int bbk_check_actions(const uint8_t* mask, const uint8_t* terminated, const uint8_t* truncated,
+                      const int64_t* actions, int64_t n, int32_t num_actions, int32_t* first_bad, void* stream) {
+    if (n <= 0) return 0;
+    util::check_actions_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        mask, terminated, truncated, actions, n, num_actions, first_bad);
+    return (int)cudaGetLastError();
+}
+
+int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int64_t n,
+                       unsigned long long* count, void* stream) {
+    if (n <= 0) return 0;
+    int64_t blocks = (n + 1023) / 1024;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    util::count_finished_kernel<<<(unsigned)blocks, 1024, 0, (cudaStream_t)stream>>>(terminated, truncated, n, count);
+    return (int)cudaGetLastError();
+}
+
+int bbk_abi_version(void) { return BBK_ABI_VERSION; }
+
+const char* bbk_build_info(void) {
+    return "libbbk: sm_100a (compute_100a)";
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+"""Device implementation of the reference's ``batch_kernel`` plugin protocol.
+
+The reference (core.py:88, 346-348, 366-368, 276-282; template
+games/tictactoe.py:71-198) expects an object with ``init(gdef, key, n,
+limit) -> V``, ``step(gdef, v, acts, key, limit) -> V`` and
+``state_at(gdef, v, i, limit) -> EnvState``, where ``V`` exposes numpy
+columns ``current_player, legal_action_mask, rewards, terminated,
+truncated, step_count, player_to_role``. Here ``V`` (``DeviceV``) owns CUDA
+tensors; the numpy columns are lazy host copies, and ``v.dev`` exposes the
+tensors themselves. Each game subclass only declares its private state and
+the C-ABI calls.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from types import SimpleNamespace
+
+import numpy as np
+
+from .. import _native as nat
+from ..core import EnvState, IllegalAction, ShapeMismatch
+from ..rng import key_state
+
+INT32_MAX = 2**31 - 1
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class DeviceV:
+    """Struct-of-arrays device state of one batch (reference V, tictactoe.py:74-79)."""
+
+    _COLS = ("current_player", "legal_action_mask", "rewards", "terminated", "truncated", "step_count",
+             "player_to_role", "observation")
+
+    def __init__(self, kern, n: int, slot0: int, device, t: int, limit: int):
+        self.kern = kern
+        self.n = n
+        self.slot0 = slot0
+        self.device = device
+        self.t = t              # batch steps since batch_init along this lineage
+        self.limit = limit
+        self.dev = SimpleNamespace()
+        self.priv = SimpleNamespace()
+        self.store = None
+        self.gen = 0
+        self._host = {}
+
+    # lazily materialised host columns (the reference reads them via getattr)
+    def _h(self, name):
+        arr = self._host.get(name)
+        if arr is None:
+            t = getattr(self.dev, name)
+            arr = t.cpu().numpy()
+            arr.flags.writeable = False
+            self._host[name] = arr
+        return arr
+
+    current_player = property(lambda self: self._h("current_player"))
+    legal_action_mask = property(lambda self: self._h("legal_action_mask"))
+    rewards = property(lambda self: self._h("rewards"))
+    terminated = property(lambda self: self._h("terminated"))
+    truncated = property(lambda self: self._h("truncated"))
+    step_count = property(lambda self: self._h("step_count"))
+    player_to_role = property(lambda self: self._h("player_to_role"))
+    observation = property(lambda self: self._h("observation"))
+
+    def priv_host(self, name):
+        key = "priv." + name
+        arr = self._host.get(key)
+        if arr is None:
+            arr = getattr(self.priv, name).cpu().numpy()
+            self._host[key] = arr
+        return arr
+
+
+class DeviceKernel:
+    """Common host logic; subclasses implement the game-specific C-ABI calls."""
+
+    game_id = ""
+    num_actions = 0
+    obs_shape: tuple = ()
+
+    # ------------------------------------------------------------ allocation
+    def new_v(self, n: int, slot0: int, device, t: int, limit: int, obs: bool = True) -> DeviceV:
+        torch = _torch()
+        v = DeviceV(self, n, slot0, device, t, limit)
+        d = v.dev
+        d.observation = torch.empty((n,) + tuple(self.obs_shape), dtype=torch.float32, device=device) if obs else None
+        d.legal_action_mask = torch.empty((n, self.num_actions), dtype=torch.bool, device=device)
+        d.rewards = torch.empty((n, 2), dtype=torch.float32, device=device)
+        d.terminated = torch.empty(n, dtype=torch.bool, device=device)
+        d.truncated = torch.empty(n, dtype=torch.bool, device=device)
+        d.current_player = torch.empty(n, dtype=torch.int32, device=device)
+        d.step_count = torch.empty(n, dtype=torch.int32, device=device)
+        d.player_to_role = torch.empty((n, 2), dtype=torch.int8, device=device)
+        self.alloc_private(v)
+        return v
+
+    def alloc_private(self, v: DeviceV) -> None:
+        raise NotImplementedError
+
+    @staticmethod
+    def cols(v: DeviceV) -> nat.Cols:
+        d = v.dev
+        return nat.Cols(nat.ptr(d.observation), nat.ptr(d.legal_action_mask), nat.ptr(d.rewards),
+                        nat.ptr(d.terminated), nat.ptr(d.truncated), nat.ptr(d.current_player),
+                        nat.ptr(d.step_count), nat.ptr(d.player_to_role))
+
+    @staticmethod
+    def _device(device):
+        torch = _torch()
+        if device is None:
+            if not torch.cuda.is_available():
+                raise nat.NativeUnavailable("no CUDA device: the engines run only on the GPU (no CPU fallback)")
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device(device)
+
+    @staticmethod
+    def _slot_keys(slot_keys, device):
+        if slot_keys is None:
+            return None
+        torch = _torch()
+        arr = np.asarray([int(k) & ((1 << 64) - 1) for k in slot_keys], dtype=np.uint64).view(np.int64)
+        return torch.from_numpy(arr).to(device)
+
+    # -------------------------------------------------------- protocol: init
+    def init(self, gdef, key, n: int, limit: int, slot_keys=None, slot0: int = 0, device=None,
+             obs: bool = True) -> DeviceV:
+        device = self._device(device)
+        v = self.new_v(n, slot0, device, 0, limit, obs)
+        sk = self._slot_keys(slot_keys, device)
+        ks = 0 if key is None else key_state(key)
+        self.launch_init(v, ks, sk)
+        return v
+
+    # -------------------------------------------------------- protocol: step
+    def as_actions(self, actions, v: DeviceV):
+        torch = _torch()
+        if isinstance(actions, torch.Tensor):
+            a = actions
+            if a.device != v.device or a.dtype != torch.int64:
+                a = a.to(device=v.device, dtype=torch.int64)
+        else:
+            arr = np.ascontiguousarray(np.asarray(actions, dtype=np.int64))
+            a = torch.from_numpy(arr).to(v.device)
+        if a.dim() != 1 or a.shape[0] != v.n:
+            raise ShapeMismatch(f"expected {v.n} actions, got shape {tuple(a.shape)}")
+        return a.contiguous()
+
+    def validate(self, v: DeviceV, a) -> None:
+        """IllegalAction with the lowest offending live slot (tictactoe.py:111-121)."""
+        torch = _torch()
+        bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device=v.device)
+        d = v.dev
+        nat.check(nat.lib().bbk_check_actions(nat.ptr(d.legal_action_mask), nat.ptr(d.terminated),
+                                              nat.ptr(d.truncated), nat.ptr(a), v.n, self.num_actions,
+                                              nat.ptr(bad), nat.stream_handle(v.device)), "bbk_check_actions")
+        slot = int(bad.item())
+        if slot != INT32_MAX:
+            act = int(a[slot].item())
+            raise IllegalAction(f"slot {slot}: illegal action {act} in {self.game_id}", action=act, slot=slot)
+
+    def step(self, gdef, v: DeviceV, actions, key, limit: int, validate: bool = True, slot_keys=None,
+             out: DeviceV | None = None) -> DeviceV:
+        a = self.as_actions(actions, v)
+        if validate:
+            self.validate(v, a)
+        sk = self._slot_keys(slot_keys, v.device)
+        ks = 0 if key is None else key_state(key)
+        if out is None:
+            out = self.new_v(v.n, v.slot0, v.device, v.t + 1, limit, v.dev.observation is not None)
+        else:
+            out.t = v.t + 1
+            out.limit = limit
+            out._host = {}
+        self.prepare_step(v, out)
+        self.launch_step(v, out, a, ks, sk, limit)
+        return out
+
+    def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
+        """Hook for games with shared append-only stores (Go)."""
+        out.store = v.store
+        out.gen = v.gen + 1
+
+    # ----------------------------------------------------- protocol: state_at
+    def host_snapshot(self, v: DeviceV) -> dict:
+        snap = v._host.get("__snap")
+        if snap is None:
+            snap = {c: getattr(v, c) for c in DeviceV._COLS if c != "observation"}
+            snap.update(self.private_host(v))
+            v._host["__snap"] = snap
+        return snap
+
+    def private_host(self, v: DeviceV) -> dict:
+        return {k: t.cpu().numpy() for k, t in vars(v.priv).items()}
+
+    def state_at(self, gdef, v: DeviceV, i: int, limit: int) -> EnvState:
+        s = self.host_snapshot(v)
+        term = bool(s["terminated"][i])
+        trunc = bool(s["truncated"][i])
+        rewards = s["rewards"][i].copy()
+        rewards.flags.writeable = False
+        mask = s["legal_action_mask"][i].copy()
+        mask.flags.writeable = False
+        p2r = (int(s["player_to_role"][i, 0]), int(s["player_to_role"][i, 1]))
+        core = self.core_view(s, i, p2r, rewards, mask, term)
+        return EnvState(
+            current_player=int(s["current_player"][i]),
+            legal_action_mask=mask,
+            rewards=rewards,
+            terminated=term,
+            truncated=trunc,
+            step_count=int(s["step_count"][i]),
+            player_to_role=p2r,
+            core=core,
+            game=gdef,
+            max_steps=limit,
+            _v=v,
+            _i=i,
+        )
+
+    def core_view(self, s: dict, i: int, p2r, rewards, mask, terminal):
+        raise NotImplementedError
+
+    @staticmethod
+    def role_rewards(p2r, rewards) -> tuple:
+        rr = [0.0, 0.0]
+        for p in range(2):
+            rr[p2r[p]] = float(rewards[p])
+        return tuple(rr)
+
+    # ----------------------------------------------------------- observation
+    def observe_at(self, gdef, v: DeviceV, i: int, role: int) -> np.ndarray:
+        torch = _torch()
+        roles = torch.full((1,), int(role), dtype=torch.uint8, device=v.device)
+        out = torch.empty((1,) + tuple(self.obs_shape), dtype=torch.float32, device=v.device)
+        self.launch_observe(v, i, roles, out)
+        arr = out[0].cpu().numpy()
+        return arr
+
+    # ---------------------------------------------------------------- slicing
+    def slice(self, gdef, v: DeviceV, i: int) -> DeviceV:
+        """One-slot copy of slot i (scalar API on a batch state)."""
+        w = self.new_v(1, v.slot0 + i, v.device, v.t, v.limit, v.dev.observation is not None)
+        for name in DeviceV._COLS:
+            src = getattr(v.dev, name)
+            if src is not None:
+                getattr(w.dev, name).copy_(src[i:i + 1])
+        for name, t in vars(v.priv).items():
+            getattr(w.priv, name).copy_(t[i:i + 1])
+        self.slice_store(v, w, i)
+        return w
+
+    def slice_store(self, v: DeviceV, w: DeviceV, i: int) -> None:
+        pass
+
+    # ------------------------------------------------------------- sampling
+    def random_actions(self, v: DeviceV, key, out=None):
+        """agents.random_actions on the device (agents.py:33-46)."""
+        torch = _torch()
+        if out is None:
+            out = torch.empty(v.n, dtype=torch.int64, device=v.device)
+        nat.check(nat.lib().bbk_random_actions(nat.ptr(v.dev.legal_action_mask), v.n, self.num_actions,
+                                               key_state(key), v.slot0, nat.ptr(out),
+                                               nat.stream_handle(v.device)), "bbk_random_actions")
+        return out
+
+    # subclasses
+    def launch_init(self, v, ks, sk):
+        raise NotImplementedError
+
+    def launch_step(self, v, out, a, ks, sk, limit):
+        raise NotImplementedError
+
+    def launch_observe(self, v, i, roles, out):
+        raise NotImplementedError

@@ -1,0 +1,195 @@
+"""Go (Tromp-Taylor, positional superko) on the device.
+
+Drop-in for reference ``games/go.py``: ``make_game(size, komi)`` returns a
+``GameDef`` with the same spec (``go_{N}x{N}``, obs (N, N, 17), N*N+1
+actions, max_steps 512; go.py:282-290) whose ``batch_kernel`` runs
+``csrc/go.cu`` through ``bbk_go_*`` (include/bbk.h).
+
+Device state per slot (besides the public columns):
+  pat[PS] int16   transposed 8-deep board history (bit 2t/2t+1: black/white
+                  stone in boards_hist[t]); replaces ``board`` + ``boards_hist``
+  hash, hist_xor int64 (u64), hist_len int32, role_to_move, pass_count u8
+and a per-lineage append-only superko store: history[hist_cap] u64 and an
+8192-bit Bloom filter. The store is shared along a trajectory; a batch up
+to two steps behind the head can still be stepped (the store is cloned and
+the filters rebuilt), older ones raise ``StaleBatch``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .. import _native as nat
+from ..core import GameDef, GameSpec, StaleBatch, UnsupportedGame
+from ._device import DeviceKernel, DeviceV, _torch
+
+HISTORY_PLANES = 8
+
+
+class GoCoreView:
+    """Host view of one slot with the reference Core's fields (go.py:83-111)."""
+
+    __slots__ = ("board", "role_to_move", "terminal", "rewards", "mask", "pass_count", "hash", "hist_xor",
+                 "hist_len", "boards_hist")
+
+    def __init__(self, board, role_to_move, terminal, rewards, mask, pass_count, hash_, hist_xor, hist_len,
+                 boards_hist):
+        self.board = board
+        self.role_to_move = role_to_move
+        self.terminal = terminal
+        self.rewards = rewards
+        self.mask = mask
+        self.pass_count = pass_count
+        self.hash = hash_
+        self.hist_xor = hist_xor
+        self.hist_len = hist_len
+        self.boards_hist = boards_hist
+
+    def encode(self) -> bytes:
+        """Byte-identical to reference Core.encode (go.py:103-111)."""
+        return (
+            self.board
+            + bytes([self.role_to_move, self.pass_count])
+            + self.hash.to_bytes(8, "little")
+            + self.hist_xor.to_bytes(8, "little")
+            + self.hist_len.to_bytes(2, "little")
+            + b"".join(self.boards_hist)
+        )
+
+
+class GoStore:
+    """Append-only per-env superko history + Bloom filter shared along a lineage."""
+
+    def __init__(self, history, bloom, hist_cap: int):
+        self.history = history
+        self.bloom = bloom
+        self.hist_cap = hist_cap
+        self.head = 0
+
+    def struct(self) -> nat.GoStore:
+        return nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
+
+
+class GoKernel(DeviceKernel):
+    def __init__(self, size: int, komi: float = 6.5):
+        if size not in (9, 13, 19):
+            raise UnsupportedGame(f"go size {size} has no device kernel (9, 13, 19 are instantiated)")
+        self.size = size
+        self.komi = float(komi)
+        self.cells = size * size
+        self.num_actions = self.cells + 1
+        self.obs_shape = (size, size, 2 * HISTORY_PLANES + 1)
+        self.game_id = f"go_{size}x{size}"
+        self.pat_stride = (self.cells + 7) & ~7
+
+    def alloc_private(self, v: DeviceV) -> None:
+        torch = _torch()
+        n, dev = v.n, v.device
+        p = v.priv
+        p.pat = torch.empty((n, self.pat_stride), dtype=torch.int16, device=dev)
+        p.hash = torch.empty(n, dtype=torch.int64, device=dev)
+        p.hist_xor = torch.empty(n, dtype=torch.int64, device=dev)
+        p.hist_len = torch.empty(n, dtype=torch.int32, device=dev)
+        p.role_to_move = torch.empty(n, dtype=torch.uint8, device=dev)
+        p.pass_count = torch.empty(n, dtype=torch.uint8, device=dev)
+
+    def state_struct(self, v: DeviceV) -> nat.GoState:
+        p = v.priv
+        return nat.GoState(nat.ptr(p.pat), nat.ptr(p.hash), nat.ptr(p.hist_xor), nat.ptr(p.hist_len),
+                           nat.ptr(p.role_to_move), nat.ptr(p.pass_count))
+
+    def new_store(self, n: int, limit: int, device) -> GoStore:
+        torch = _torch()
+        cap = int(limit) + 2
+        hist = torch.empty((n, cap), dtype=torch.int64, device=device)
+        bloom = torch.empty((n, 256), dtype=torch.int32, device=device)
+        return GoStore(hist, bloom, cap)
+
+    def launch_init(self, v: DeviceV, ks: int, sk) -> None:
+        v.store = self.new_store(v.n, v.limit, v.device)
+        v.gen = 0
+        v.store.head = 0
+        cols, st, store = self.cols(v), self.state_struct(v), v.store.struct()
+        nat.check(nat.lib().bbk_go_init(self.size, cols, st, store, v.n, v.slot0, ks, nat.ptr(sk), v.limit,
+                                        nat.stream_handle(v.device)), "bbk_go_init")
+
+    def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
+        store = v.store
+        if out.limit + 2 > store.hist_cap:
+            raise ValueError("max_steps exceeds the history capacity of this batch")
+        if v.gen != store.head:
+            if store.head - v.gen > 2:
+                raise StaleBatch(f"batch is {store.head - v.gen} steps behind its lineage; only the last two "
+                                 "predecessors can be stepped again")
+            # branch: private copy of the history, filters rebuilt for v's lengths
+            store = GoStore(store.history.clone(), store.bloom.clone(), store.hist_cap)
+            store.head = v.gen
+            nat.check(nat.lib().bbk_go_rebuild_bloom(store.struct(), nat.ptr(v.priv.hist_len), v.n,
+                                                     nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
+        out.store = store
+        out.gen = v.gen + 1
+        store.head = out.gen
+
+    def launch_step(self, v, out, a, ks, sk, limit) -> None:
+        nat.check(nat.lib().bbk_go_step(self.size, self.komi, self.cols(v), self.state_struct(v), self.cols(out),
+                                        self.state_struct(out), out.store.struct(), nat.ptr(a), v.n, v.slot0, ks,
+                                        nat.ptr(sk), limit, nat.stream_handle(v.device)), "bbk_go_step")
+
+    def launch_observe(self, v, i, roles, out) -> None:
+        nat.check(nat.lib().bbk_go_observe(self.size, nat.ptr(v.priv.pat[i:i + 1]), nat.ptr(roles), nat.ptr(out), 1,
+                                           nat.stream_handle(v.device)), "bbk_go_observe")
+
+    def observe_at(self, gdef, v, i, role):
+        if v.dev.observation is not None and int(role) == int(self.host_snapshot(v)["role_to_move"][i]):
+            return v.observation[i].copy()
+        return super().observe_at(gdef, v, i, role)
+
+    def slice_store(self, v: DeviceV, w: DeviceV, i: int) -> None:
+        s = v.store
+        w.store = GoStore(s.history[i:i + 1].clone(), s.bloom[i:i + 1].clone(), s.hist_cap)
+        w.gen = 0
+        w.store.head = 0
+        if v.gen != s.head:
+            if s.head - v.gen > 2:
+                raise StaleBatch("batch too far behind its lineage to slice")
+            nat.check(nat.lib().bbk_go_rebuild_bloom(w.store.struct(), nat.ptr(w.priv.hist_len), 1,
+                                                     nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
+
+    def core_view(self, s, i, p2r, rewards, mask, terminal):
+        pat = s["pat"][i].view(np.uint16)[: self.cells].astype(np.uint32)
+        step = int(s["step_count"][i])
+        nbh = min(step + 1, HISTORY_PLANES)
+        boards = []
+        for t in range(nbh):
+            b = ((pat >> (2 * t)) & 1) + 2 * ((pat >> (2 * t + 1)) & 1)
+            boards.append(b.astype(np.uint8).tobytes())
+        bits = 0 if (terminal or s["truncated"][i]) else int.from_bytes(
+            np.packbits(mask, bitorder="little").tobytes(), "little")
+        return GoCoreView(
+            board=boards[0],
+            role_to_move=int(s["role_to_move"][i]),
+            terminal=terminal,
+            rewards=self.role_rewards(p2r, rewards),
+            mask=bits,
+            pass_count=int(s["pass_count"][i]),
+            hash_=int(s["hash"][i]) & ((1 << 64) - 1),
+            hist_xor=int(s["hist_xor"][i]) & ((1 << 64) - 1),
+            hist_len=int(s["hist_len"][i]),
+            boards_hist=tuple(boards),
+        )
+
+
+def make_game(size: int = 9, komi: float = 6.5, allow_self_capture: bool = False) -> GameDef:
+    """Device twin of reference go.make_game (go.py:114-290)."""
+    if allow_self_capture:
+        raise UnsupportedGame("allow_self_capture=True has no device kernel (reference default is False)")
+    cells = size * size
+    return GameDef(
+        spec=GameSpec(f"go_{size}x{size}", 2, (size, size, 2 * HISTORY_PLANES + 1), cells + 1),
+        max_steps=512,
+        batch_kernel=GoKernel(size, komi),
+    )
+
+
+GAME = make_game(9)
+GAME19 = make_game(19)

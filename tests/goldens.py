@@ -1,0 +1,24 @@
+"""Helpers for the committed golden fixtures (tests/golden/*.json, made by make_golden.py)."""
+
+import hashlib
+import json
+import os
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def names():
+    return sorted(f[:-5] for f in os.listdir(HERE) if f.endswith(".json"))
+
+
+def load(name):
+    with open(os.path.join(HERE, name + ".json")) as fh:
+        return json.load(fh)
+
+
+def digest(b: bytes) -> str:
+    return hashlib.blake2b(b, digest_size=16).hexdigest()
+
+
+def game_args(rec):
+    return rec["game_id"], rec["batch"], rec["seed"], rec["max_steps"]
