@@ -108,6 +108,28 @@ int bbk_bg_step(const bbk_cols* in, const bbk_bg_state* in_s, const bbk_cols* ou
                 const uint64_t* slot_keys, int32_t max_steps, void* stream);
 int bbk_bg_observe(const bbk_bg_state* s, const uint8_t* role, float* obs, int64_t n, void* stream);
 
+/* --------------------------------------------------------------- Chess --
+ * No reference engine (reserved spec, games/__init__.py:23); rules and
+ * encodings per PAPER.md:781-856 and DESIGN.md §3.3 (CPU twin:
+ * oracle/orc_chess.c, perft-pinned).
+ *   board[n, 64]  piece code per square (a1 = 0; colour << 3 | P1 N2 B3 R4 Q5 K6)
+ *   misc[n, 8]    stm, castling bits, ep square (255 = none), half-move clock, repetition
+ *   hist[n, 4608] per-env ring of 128 plies: packed boards (32 B) + meta (u32),
+ *                 shared along a trajectory (in place). */
+typedef struct bbk_chess_state {
+    uint8_t* board;
+    uint8_t* misc;
+    uint8_t* hist;
+} bbk_chess_state;
+
+int bbk_chess_init(const bbk_cols* out, const bbk_chess_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
+                   const uint64_t* slot_keys, int32_t max_steps, void* stream);
+int bbk_chess_step(const bbk_cols* in, const bbk_chess_state* in_s, const bbk_cols* out, const bbk_chess_state* out_s,
+                   const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                   int32_t max_steps, void* stream);
+int bbk_chess_observe(const bbk_chess_state* s, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n,
+                      void* stream);
+
 /* ------------------------------------------------------------- generic --
  * agents.random_actions (agents.py:33-46): a_i = index of the d-th legal
  * action, d = child(key, slot0+i) % max(popcount(mask_i), 1); 0 if none. */

@@ -66,6 +66,8 @@ def lib():
             L.orc_chess_new.restype = _P
             L.orc_chess_perft.argtypes = [C.c_char_p, C.c_int]
             L.orc_chess_perft.restype = C.c_uint64
+            L.orc_chess_set_fen.argtypes = [_P, _I64, C.c_char_p]
+            L.orc_chess_set_fen.restype = C.c_int
         if hasattr(L, "orc_shogi_new"):
             L.orc_shogi_new.argtypes = [_I64, C.c_int]
             L.orc_shogi_new.restype = _P
@@ -258,6 +260,13 @@ class ChessBatch(_Batch):
 
     def __init__(self, n: int, max_steps: int = 256):
         super().__init__(lib().orc_chess_new(n, max_steps), n)
+
+    def set_fen(self, i: int, fen: str):
+        assert self.L.orc_chess_set_fen(self.h, i, fen.encode()) == 0
+
+    @staticmethod
+    def perft(fen: str, depth: int) -> int:
+        return int(lib().orc_chess_perft(fen.encode(), depth))
 
 
 class ShogiBatch(_Batch):

@@ -433,6 +433,9 @@ static int parse_fen(const char* fen, cpos* p) {
     }
     if (*c) c++;
     if (*c && *c != '-') { p->ep = (int8_t)((c[1] - '1') * 8 + (c[0] - 'a')); }
+    while (*c && *c != ' ') c++;
+    if (*c) c++;
+    if (*c >= '0' && *c <= '9') p->halfmove = (uint8_t)atoi(c);
     return 0;
 }
 

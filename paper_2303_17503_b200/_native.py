@@ -77,7 +77,7 @@ def _declare(L):
         if hasattr(L, f"bbk_{g}_step"):
             getattr(L, f"bbk_{g}_init").argtypes = [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P]
             getattr(L, f"bbk_{g}_step").argtypes = [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P]
-            getattr(L, f"bbk_{g}_observe").argtypes = [ptr(S), P, P, I64, P]
+            getattr(L, f"bbk_{g}_observe").argtypes = [ptr(S), P, P, P, I64, P]
     for name in dir(L):
         pass
     return L

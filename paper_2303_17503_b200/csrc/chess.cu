@@ -1,0 +1,623 @@
+// Chess batched step for sm_100a (no reference engine: PAPER.md:781-856 +
+// DESIGN.md §3.3 conventions; CPU twin oracle/orc_chess.c, perft-pinned).
+//
+// One warp per board. Lane l owns squares l and l+32 of the 64-byte board in
+// shared memory. Per step:
+//   1. lane 0 applies the action (AlphaZero 64x73 code in the mover's frame);
+//   2. legal moves of the side to move, check/pin filtered: the opponent's
+//      attack map (king removed) is an OR-reduction of per-lane ray scans;
+//      lanes 0-7 walk the 8 rays out of the king to find checkers, block
+//      squares and pins, lanes 8-17 test knight/pawn checkers; every lane
+//      then emits its pieces' moves into a 4672-byte mask staged in shared
+//      memory (en passant gets a full discovered-check test);
+//   3. repetition: lanes compare the packed position against the ring
+//      entries inside the half-move window in parallel (threefold = draw),
+//      then mate / stalemate / insufficient material / 50-move rule;
+//   4. observation: the 8 x 8 x 119 record is 7616 floats, almost all 0/1.
+//      Lanes build it as a 7616-bit stream in shared memory (even squares,
+//      then odd squares, so no two lanes touch one word), and emit float4
+//      chunks through a 16-entry LUT; the two count planes are patched in.
+#include "common.cuh"
+#include "../../include/bbk.h"
+
+namespace chess {
+using namespace bbk;
+
+constexpr int A = 4672;
+constexpr int NF = 8 * 8 * 119;      // floats per record (7616)
+constexpr int RING = 128;
+constexpr int HIST_BYTES = RING * 32 + RING * 4;   // per env: packed boards + meta
+constexpr int kWarps = 4;
+
+enum { EMPTY = 0, P = 1, N = 2, B = 3, R = 4, Q = 5, K = 6 };
+
+__device__ __constant__ int8_t KN_DR[8] = {2, 1, -1, -2, -2, -1, 1, 2};
+__device__ __constant__ int8_t KN_DF[8] = {1, 2, 2, 1, -1, -2, -2, -1};
+__device__ __constant__ int8_t DIR_DR[8] = {1, 1, 0, -1, -1, -1, 0, 1};
+__device__ __constant__ int8_t DIR_DF[8] = {0, 1, 1, 1, 0, -1, -1, -1};
+
+struct WarpSmem {
+    alignas(16) uint8_t mask[A + 16];
+    alignas(16) uint32_t bits[NF / 32 + 4];
+    alignas(16) uint8_t bd[64];
+    alignas(16) uint8_t packed[32];
+    alignas(16) uint8_t past[8][64];   // boards of history steps t = 0..7 (absolute squares)
+    uint8_t prep[8];
+    uint64_t pinray[8];
+    int8_t pinsq[8];
+};
+
+struct Params {
+    bbk_cols in, out;
+    bbk_chess_state in_s, out_s;
+    const int64_t* actions;
+    const uint64_t* slot_keys;
+    int64_t n, slot0;
+    uint64_t key;
+    int32_t max_steps;
+    int force_reset;
+};
+
+__device__ __forceinline__ bool on(int r, int f) { return (unsigned)r < 8u && (unsigned)f < 8u; }
+__device__ __forceinline__ int color(uint8_t pc) { return pc >> 3; }
+__device__ __forceinline__ int type(uint8_t pc) { return pc & 7; }
+__device__ __forceinline__ uint8_t mk(int c, int t) { return (uint8_t)((c << 3) | t); }
+
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+    uint32_t lo = __reduce_or_sync(BBK_FULL, (uint32_t)v), hi = __reduce_or_sync(BBK_FULL, (uint32_t)(v >> 32));
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// Attack test on a modified board (en passant legality): is `sq` attacked by
+// side `by` when squares e1/e2 are emptied and `add` holds `add_pc`?
+__device__ bool attacked_mod(const uint8_t* bd, int sq, int by, int e1, int e2, int add, uint8_t add_pc) {
+    auto at = [&](int s) -> uint8_t { return s == add ? add_pc : (s == e1 || s == e2) ? (uint8_t)0 : bd[s]; };
+    int r = sq >> 3, f = sq & 7;
+    int pr = by == 0 ? r - 1 : r + 1;
+    for (int df = -1; df <= 1; df += 2)
+        if (on(pr, f + df) && at(pr * 8 + f + df) == mk(by, P)) return true;
+    for (int k = 0; k < 8; k++) {
+        int rr = r + KN_DR[k], ff = f + KN_DF[k];
+        if (on(rr, ff) && at(rr * 8 + ff) == mk(by, N)) return true;
+    }
+    for (int d = 0; d < 8; d++) {
+        int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+        if (on(rr, ff) && at(rr * 8 + ff) == mk(by, K)) return true;
+        bool diag = DIR_DR[d] != 0 && DIR_DF[d] != 0;
+        while (on(rr, ff)) {
+            uint8_t pc = at(rr * 8 + ff);
+            if (pc) {
+                if (color(pc) == by && (type(pc) == Q || type(pc) == (diag ? B : R))) return true;
+                break;
+            }
+            rr += DIR_DR[d]; ff += DIR_DF[d];
+        }
+    }
+    return false;
+}
+
+// AlphaZero action index in the mover's frame.
+__device__ __forceinline__ int action_of(int fl, int from, int to, int promo) {
+    int f = from ^ fl, t = to ^ fl;
+    int dr = (t >> 3) - (f >> 3), df = (t & 7) - (f & 7);
+    int plane;
+    if (promo && promo != Q) {
+        plane = 64 + 3 * (promo == N ? 0 : promo == B ? 1 : 2) + (df + 1);
+    } else {
+        int adr = dr < 0 ? -dr : dr, adf = df < 0 ? -df : df;
+        if ((adr == 2 && adf == 1) || (adr == 1 && adf == 2)) {
+            int k = 0;
+            for (int j = 0; j < 8; j++) if (KN_DR[j] == dr && KN_DF[j] == df) k = j;
+            plane = 56 + k;
+        } else {
+            int dist = adr > adf ? adr : adf;
+            int sr = (dr > 0) - (dr < 0), sf = (df > 0) - (df < 0);
+            int d = 0;
+            for (int j = 0; j < 8; j++) if (DIR_DR[j] == sr && DIR_DF[j] == sf) d = j;
+            plane = d * 7 + dist - 1;
+        }
+    }
+    return f * 73 + plane;
+}
+
+struct MoveCtx {
+    const uint8_t* bd;
+    uint8_t* mask;
+    int side, fl, ksq;
+    uint64_t att;        // opponent attacks with our king removed
+    uint64_t checkmask;  // legal destinations for non-king moves
+    const int8_t* pinsq;
+    const uint64_t* pinray;
+    int ep;
+};
+
+__device__ __forceinline__ uint64_t pin_of(const MoveCtx& c, int s) {
+    uint64_t r = ~0ull;
+#pragma unroll
+    for (int d = 0; d < 8; d++) if (c.pinsq[d] == s) r = c.pinray[d];
+    return r;
+}
+
+// Emit the legal moves of our piece on `s`; returns (count, ep_legal).
+__device__ int gen_square(const MoveCtx& c, int s, bool& ep_legal) {
+    const uint8_t pc = c.bd[s];
+    if (!pc || color(pc) != c.side) return 0;
+    const int t = type(pc), r = s >> 3, f = s & 7, side = c.side;
+    int cnt = 0;
+    if (t == K) {
+        for (int d = 0; d < 8; d++) {
+            int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+            if (!on(rr, ff)) continue;
+            int to = rr * 8 + ff;
+            uint8_t q = c.bd[to];
+            if (q && color(q) == side) continue;
+            if ((c.att >> to) & 1ull) continue;
+            c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
+        }
+        return cnt;   // castling handled by the caller (needs rights)
+    }
+    const uint64_t allow = c.checkmask & pin_of(c, s);
+    if (t == P) {
+        const int dr = side == 0 ? 1 : -1, last = side == 0 ? 7 : 0, start = side == 0 ? 1 : 6;
+        const int r1 = r + dr;
+        if (!on(r1, f)) return 0;
+        auto emit = [&](int to) {
+            if (r1 == last) {
+                c.mask[action_of(c.fl, s, to, Q)] = 1;
+                c.mask[action_of(c.fl, s, to, R)] = 1;
+                c.mask[action_of(c.fl, s, to, B)] = 1;
+                c.mask[action_of(c.fl, s, to, N)] = 1;
+                cnt += 4;
+            } else {
+                c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
+            }
+        };
+        const int to1 = r1 * 8 + f;
+        if (!c.bd[to1]) {
+            if ((allow >> to1) & 1ull) emit(to1);
+            const int to2 = (r + 2 * dr) * 8 + f;
+            if (r == start && !c.bd[to2] && ((allow >> to2) & 1ull)) emit(to2);
+        }
+        for (int df = -1; df <= 1; df += 2) {
+            if (!on(r1, f + df)) continue;
+            const int to = r1 * 8 + f + df;
+            const uint8_t q = c.bd[to];
+            if (q && color(q) != side) {
+                if ((allow >> to) & 1ull) emit(to);
+            } else if (to == c.ep) {
+                const int cap = side == 0 ? to - 8 : to + 8;
+                if (!attacked_mod(c.bd, c.ksq, 1 - side, s, cap, to, pc)) {
+                    c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
+                    ep_legal = true;
+                }
+            }
+        }
+        return cnt;
+    }
+    if (t == N) {
+        for (int k = 0; k < 8; k++) {
+            int rr = r + KN_DR[k], ff = f + KN_DF[k];
+            if (!on(rr, ff)) continue;
+            int to = rr * 8 + ff;
+            uint8_t q = c.bd[to];
+            if ((q && color(q) == side) || !((allow >> to) & 1ull)) continue;
+            c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
+        }
+        return cnt;
+    }
+    const int d0 = t == B ? 1 : 0, stp = (t == B || t == R) ? 2 : 1;
+    for (int d = d0; d < 8; d += stp) {
+        int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+        while (on(rr, ff)) {
+            int to = rr * 8 + ff;
+            uint8_t q = c.bd[to];
+            if (q && color(q) == side) break;
+            if ((allow >> to) & 1ull) { c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++; }
+            if (q) break;
+            rr += DIR_DR[d]; ff += DIR_DF[d];
+        }
+    }
+    return cnt;
+}
+
+// Attacks of the opponent piece on `s` (king `ksq` transparent to sliders).
+__device__ uint64_t attacks_from(const uint8_t* bd, int s, int by, int ksq) {
+    const uint8_t pc = bd[s];
+    if (!pc || color(pc) != by) return 0ull;
+    const int t = type(pc), r = s >> 3, f = s & 7;
+    uint64_t a = 0ull;
+    if (t == P) {
+        int rr = by == 0 ? r + 1 : r - 1;
+        if (on(rr, f - 1)) a |= 1ull << (rr * 8 + f - 1);
+        if (on(rr, f + 1)) a |= 1ull << (rr * 8 + f + 1);
+    } else if (t == N) {
+        for (int k = 0; k < 8; k++) { int rr = r + KN_DR[k], ff = f + KN_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+    } else if (t == K) {
+        for (int d = 0; d < 8; d++) { int rr = r + DIR_DR[d], ff = f + DIR_DF[d]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+    } else {
+        const int d0 = t == B ? 1 : 0, stp = (t == B || t == R) ? 2 : 1;
+        for (int d = d0; d < 8; d += stp) {
+            int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+            while (on(rr, ff)) {
+                int to = rr * 8 + ff;
+                a |= 1ull << to;
+                if (bd[to] && to != ksq) break;
+                rr += DIR_DR[d]; ff += DIR_DF[d];
+            }
+        }
+    }
+    return a;
+}
+
+// Apply a move encoded in the mover's frame (mirrors oracle make()).
+__device__ void apply_action(uint8_t* bd, int& stm, int& castle, int& ep, int& halfmove, int a) {
+    const int fl = stm ? 56 : 0;
+    const int fromv = a / 73, plane = a - 73 * fromv;
+    int dr, df, promo = 0;
+    if (plane < 56) { int d = plane / 7, dist = plane - 7 * d + 1; dr = DIR_DR[d] * dist; df = DIR_DF[d] * dist; }
+    else if (plane < 64) { dr = KN_DR[plane - 56]; df = KN_DF[plane - 56]; }
+    else { int u = plane - 64; promo = u / 3 == 0 ? N : u / 3 == 1 ? B : R; df = u % 3 - 1; dr = 1; }
+    const int tov = fromv + dr * 8 + df;
+    const int from = fromv ^ fl, to = tov ^ fl;
+    const uint8_t pc = bd[from], cap = bd[to];
+    const int side = color(pc), t = type(pc);
+    const bool reset = t == P || cap != EMPTY;
+    if (t == P && !promo && ((to >> 3) == 7 || (to >> 3) == 0)) promo = Q;
+    if (t == P && to == ep && cap == EMPTY && (from & 7) != (to & 7)) bd[side == 0 ? to - 8 : to + 8] = EMPTY;
+    bd[to] = promo ? mk(side, promo) : pc;
+    bd[from] = EMPTY;
+    if (t == K && ((to & 7) - (from & 7) == 2 || (from & 7) - (to & 7) == 2)) {
+        int rank = from & ~7;
+        if ((to & 7) == 6) { bd[rank + 5] = bd[rank + 7]; bd[rank + 7] = EMPTY; }
+        else { bd[rank + 3] = bd[rank + 0]; bd[rank + 0] = EMPTY; }
+    }
+    auto clr = [](int s) -> int { return s == 0 ? 2 : s == 4 ? 3 : s == 7 ? 1 : s == 56 ? 8 : s == 60 ? 12 : s == 63 ? 4 : 0; };
+    castle &= ~(clr(from) | clr(to));
+    ep = -1;
+    if (t == P && (to - from == 16 || from - to == 16)) ep = (from + to) / 2;
+    halfmove = reset ? 0 : halfmove + 1;
+    stm ^= 1;
+}
+
+__device__ __forceinline__ void load_past(uint8_t* dst, const uint8_t* hist_env, int ply, int lane) {
+    // packed nibble board of ply -> 64 piece bytes (absolute squares)
+    const uint8_t* src = hist_env + (ply & (RING - 1)) * 32;
+    uint8_t byte = src[lane];
+    dst[2 * lane] = byte & 15;
+    dst[2 * lane + 1] = byte >> 4;
+}
+
+__global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
+    __shared__ WarpSmem sm[kWarps];
+    __shared__ float4 lut[16];
+    if (threadIdx.x < 16) {
+        uint32_t q = threadIdx.x;
+        lut[q] = make_float4((float)(q & 1), (float)((q >> 1) & 1), (float)((q >> 2) & 1), (float)((q >> 3) & 1));
+    }
+    __syncthreads();
+    WarpSmem& S = sm[threadIdx.x >> 5];
+    const int lane = lane_id();
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
+        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+        const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
+        uint8_t* hist = p.out_s.hist + b * (int64_t)HIST_BYTES;
+        uint32_t* hmeta = reinterpret_cast<uint32_t*>(hist + RING * 32);
+        int8_t p2r0, p2r1;
+        int stm, castle, ep, halfmove, step;
+        if (reset) {
+            int c = (int)(child(k, 0) % 2ull);
+            p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
+            const uint8_t back[8] = {R, N, B, Q, K, B, N, R};
+            for (int s = lane; s < 64; s += 32) {
+                int r = s >> 3, f = s & 7;
+                uint8_t v = r == 0 ? mk(0, back[f]) : r == 1 ? mk(0, P) : r == 6 ? mk(1, P) : r == 7 ? mk(1, back[f]) : 0;
+                S.bd[s] = v;
+            }
+            stm = 0; castle = 15; ep = -1; halfmove = 0; step = 0;
+        } else {
+            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
+            const uint8_t* ib = p.in_s.board + b * 64;
+            S.bd[lane] = ib[lane]; S.bd[lane + 32] = ib[lane + 32];
+            const uint8_t* m = p.in_s.misc + b * 8;
+            stm = m[0]; castle = m[1]; ep = (int8_t)m[2]; halfmove = m[3];
+            step = p.in.step_count[b] + 1;
+            __syncwarp();
+            if (lane == 0) apply_action(S.bd, stm, castle, ep, halfmove, (int)p.actions[b]);
+            stm = __shfl_sync(BBK_FULL, stm, 0); castle = __shfl_sync(BBK_FULL, castle, 0);
+            ep = __shfl_sync(BBK_FULL, ep, 0); halfmove = __shfl_sync(BBK_FULL, halfmove, 0);
+        }
+        // zero the mask staging area while the board settles
+        for (int i = lane; i < A / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        const int side = stm, opp = 1 - side, fl = side ? 56 : 0;
+        // ---- king, attack map, checks, pins
+        const unsigned kb0 = __ballot_sync(BBK_FULL, S.bd[lane] == mk(side, K));
+        const unsigned kb1 = __ballot_sync(BBK_FULL, S.bd[lane + 32] == mk(side, K));
+        const int ksq = kb0 ? __ffs(kb0) - 1 : kb1 ? 32 + __ffs(kb1) - 1 : 0;
+        const uint64_t att = warp_or64(attacks_from(S.bd, lane, opp, ksq) | attacks_from(S.bd, lane + 32, opp, ksq));
+        const bool in_check = (att >> ksq) & 1ull;
+        bool checker = false;
+        uint64_t block = 0ull;
+        if (lane < 8) {          // ray d = lane out of the king
+            const int d = lane;
+            const bool diag = DIR_DR[d] != 0 && DIR_DF[d] != 0;
+            int rr = (ksq >> 3) + DIR_DR[d], ff = (ksq & 7) + DIR_DF[d];
+            uint64_t ray = 0ull;
+            int own = -1;
+            int8_t pin = -1;
+            uint64_t pray = 0ull;
+            while (on(rr, ff)) {
+                int s = rr * 8 + ff;
+                ray |= 1ull << s;
+                uint8_t pc = S.bd[s];
+                if (pc) {
+                    bool slider = color(pc) == opp && (type(pc) == Q || type(pc) == (diag ? B : R));
+                    if (own < 0) {
+                        if (color(pc) == side) own = s;
+                        else { if (slider) { checker = true; block = ray; } break; }
+                    } else {
+                        if (slider) { pin = (int8_t)own; pray = ray; }
+                        break;
+                    }
+                }
+                rr += DIR_DR[d]; ff += DIR_DF[d];
+            }
+            S.pinsq[d] = pin;
+            S.pinray[d] = pray;
+        } else if (lane < 16) {  // knight checkers
+            const int j = lane - 8;
+            int rr = (ksq >> 3) + KN_DR[j], ff = (ksq & 7) + KN_DF[j];
+            if (on(rr, ff) && S.bd[rr * 8 + ff] == mk(opp, N)) { checker = true; block = 1ull << (rr * 8 + ff); }
+        } else if (lane < 18) {  // pawn checkers
+            int rr = (ksq >> 3) + (side == 0 ? 1 : -1), ff = (ksq & 7) + (lane == 16 ? -1 : 1);
+            if (on(rr, ff) && S.bd[rr * 8 + ff] == mk(opp, P)) { checker = true; block = 1ull << (rr * 8 + ff); }
+        }
+        const int nchecks = __popc(__ballot_sync(BBK_FULL, checker));
+        const uint64_t blockall = warp_or64(block);
+        __syncwarp();
+        MoveCtx c;
+        c.bd = S.bd; c.mask = S.mask; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att;
+        c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
+        c.pinsq = S.pinsq; c.pinray = S.pinray; c.ep = ep;
+        bool ep_legal = false;
+        int cnt = gen_square(c, lane, ep_legal) + gen_square(c, lane + 32, ep_legal);
+        if (lane == 0 && !in_check) {   // castling (oracle gen_pseudo castling rules)
+            const int rank = side == 0 ? 0 : 56, kbit = side == 0 ? 1 : 4, qbit = side == 0 ? 2 : 8;
+            if (ksq == rank + 4) {
+                if ((castle & kbit) && S.bd[rank + 7] == mk(side, R) && !S.bd[rank + 5] && !S.bd[rank + 6] &&
+                    !((att >> (rank + 5)) & 1ull) && !((att >> (rank + 6)) & 1ull)) {
+                    S.mask[action_of(fl, ksq, rank + 6, 0)] = 1; cnt++;
+                }
+                if ((castle & qbit) && S.bd[rank + 0] == mk(side, R) && !S.bd[rank + 1] && !S.bd[rank + 2] &&
+                    !S.bd[rank + 3] && !((att >> (rank + 3)) & 1ull) && !((att >> (rank + 2)) & 1ull)) {
+                    S.mask[action_of(fl, ksq, rank + 2, 0)] = 1; cnt++;
+                }
+            }
+        }
+        const int nlegal = warp_sum(cnt);
+        const bool any_ep = __any_sync(BBK_FULL, ep_legal);
+        const int ep_eff = any_ep ? ep : -1;
+        // ---- packed position + repetition within the half-move window
+        {
+            uint8_t byte = (uint8_t)(S.bd[2 * lane] | (S.bd[2 * lane + 1] << 4));
+            S.packed[lane] = byte;
+        }
+        __syncwarp();
+        const uint32_t meta_key = (uint32_t)side | ((uint32_t)castle << 8) | ((uint32_t)(uint8_t)ep_eff << 16);
+        int reps = 0;
+        const int window = halfmove < step ? halfmove : step;
+        for (int j = lane; 2 * (j + 1) <= window; j += 32) {
+            const int ply = step - 2 * (j + 1);
+            const uint32_t m = hmeta[ply & (RING - 1)];
+            if ((m & 0xFFFFFFu) == meta_key) {
+                const uint4* hb = reinterpret_cast<const uint4*>(hist + (ply & (RING - 1)) * 32);
+                const uint4* cb = reinterpret_cast<const uint4*>(S.packed);
+                uint4 x0 = hb[0], x1 = hb[1], y0 = cb[0], y1 = cb[1];
+                if (x0.x == y0.x && x0.y == y0.y && x0.z == y0.z && x0.w == y0.w && x1.x == y1.x && x1.y == y1.y &&
+                    x1.z == y1.z && x1.w == y1.w) reps++;
+            }
+        }
+        reps = warp_sum(reps);
+        const int rep = reps > 2 ? 2 : reps;
+        // ---- insufficient material (oracle insufficient())
+        int minors = 0, heavy = 0, knights = 0, blight = 0, bdark = 0;
+        for (int s = lane; s < 64; s += 32) {
+            uint8_t pc = S.bd[s];
+            int t = type(pc);
+            if (!pc || t == K) continue;
+            if (t == P || t == R || t == Q) heavy++;
+            else {
+                minors++;
+                if (t == N) knights++;
+                else if ((((s >> 3) + (s & 7)) & 1)) blight++;
+                else bdark++;
+            }
+        }
+        heavy = warp_sum(heavy); minors = warp_sum(minors); knights = warp_sum(knights);
+        blight = warp_sum(blight); bdark = warp_sum(bdark);
+        const bool insufficient = heavy == 0 && (minors <= 1 || (knights == 0 && (blight == 0 || bdark == 0)));
+        bool terminal = false;
+        float rr0 = 0.0f, rr1 = 0.0f;
+        if (nlegal == 0) {
+            terminal = true;
+            if (in_check) { if (side == 0) { rr0 = -1.0f; rr1 = 1.0f; } else { rr0 = 1.0f; rr1 = -1.0f; } }
+        } else if (insufficient || halfmove >= 100 || reps >= 2) {
+            terminal = true;
+        }
+        const bool truncated = !terminal && step >= p.max_steps;
+        // ---- history entry for this ply, then the past boards for the observation
+        if (lane < 2) reinterpret_cast<uint4*>(hist + (step & (RING - 1)) * 32)[lane] =
+            reinterpret_cast<const uint4*>(S.packed)[lane];
+        if (lane == 0) hmeta[step & (RING - 1)] = meta_key | ((uint32_t)rep << 24);
+        S.past[0][lane] = S.bd[lane]; S.past[0][lane + 32] = S.bd[lane + 32];
+        for (int t = 1; t < 8; t++) {
+            if (step - t >= 0) {
+                load_past(S.past[t], hist, step - t, lane);
+                if (lane == 0) S.prep[t] = (uint8_t)(hmeta[(step - t) & (RING - 1)] >> 24);
+            } else {
+                S.past[t][lane] = 0; S.past[t][lane + 32] = 0;
+                if (lane == 0) S.prep[t] = 0;
+            }
+        }
+        if (lane == 0) S.prep[0] = (uint8_t)rep;
+        for (int i = lane; i < NF / 32 + 4; i += 32) S.bits[i] = 0u;
+        __syncwarp();
+        // ---- observation bitstream: square v (mover frame) owns bits [119 v, 119 v + 119)
+        const int own_k = side ? 4 : 1, own_q = side ? 8 : 2, opp_k = side ? 1 : 4, opp_q = side ? 2 : 8;
+        const uint32_t cbits = ((uint32_t)side << 0) | ((uint32_t)((castle & own_k) != 0) << 2) |
+                               ((uint32_t)((castle & own_q) != 0) << 3) | ((uint32_t)((castle & opp_k) != 0) << 4) |
+                               ((uint32_t)((castle & opp_q) != 0) << 5);   // planes 112.. relative
+#pragma unroll
+        for (int pass = 0; pass < 2; pass++) {
+            const int v = 2 * lane + pass;
+            const int sabs = v ^ fl;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};   // 119-bit pattern of square v (bit k = plane k)
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                uint8_t pc = S.past[t][sabs];
+                int base = 14 * t;
+                if (pc) {
+                    int bit = base + (color(pc) == side ? 0 : 6) + type(pc) - 1;
+                    w[bit >> 5] |= 1u << (bit & 31);
+                }
+                uint8_t rp = S.prep[t];
+                if (rp >= 1) w[(base + 12) >> 5] |= 1u << ((base + 12) & 31);
+                if (rp >= 2) w[(base + 13) >> 5] |= 1u << ((base + 13) & 31);
+            }
+            // planes 112.. : colour, [113 count], castling x4, [118 count]
+            w[3] |= cbits << (112 - 96);
+            // OR the 119-bit pattern into the stream at bit offset 119 v
+            const int off = 119 * v, wi = off >> 5, sh = off & 31;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                uint32_t lo = w[j] << sh;
+                uint32_t hi = sh ? (w[j] >> (32 - sh)) : 0u;
+                S.bits[wi + j] |= lo;
+                if (hi) S.bits[wi + j + 1] |= hi;
+            }
+            __syncwarp();
+        }
+        const float cnt113 = (float)step / 512.0f, cnt118 = (float)halfmove / 100.0f;
+        if (p.out.observation) {
+            float4* o4 = reinterpret_cast<float4*>(p.out.observation + b * (int64_t)NF);
+            for (int j = lane; j < NF / 4; j += 32) {
+                const uint32_t nib = (S.bits[j >> 3] >> ((j & 7) * 4)) & 15u;
+                float4 val = lut[nib];
+                const uint32_t f0 = 4u * (uint32_t)j;
+                const uint32_t cc = (f0 * 8812u) >> 20;      // f0 / 119 (exact for f0 < 7616+)
+                const int k0 = (int)(f0 - 119u * cc);
+                float* vp = reinterpret_cast<float*>(&val);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    int kq = k0 + q;
+                    if (kq >= 119) kq -= 119;
+                    if (kq == 113) vp[q] = cnt113;
+                    else if (kq == 118) vp[q] = cnt118;
+                }
+                o4[j] = val;
+            }
+        }
+        // ---- mask: zero when finished, else the staged bytes
+        if (terminal || truncated) {
+            for (int i = lane; i < A / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+        }
+        uint4* m4 = reinterpret_cast<uint4*>(p.out.legal_action_mask + b * (int64_t)A);
+        for (int i = lane; i < A / 16; i += 32) m4[i] = reinterpret_cast<const uint4*>(S.mask)[i];
+        uint8_t* ob = p.out_s.board + b * 64;
+        ob[lane] = S.bd[lane]; ob[lane + 32] = S.bd[lane + 32];
+        if (lane == 0) {
+            uint8_t* m = p.out_s.misc + b * 8;
+            m[0] = (uint8_t)stm; m[1] = (uint8_t)castle; m[2] = (uint8_t)ep; m[3] = (uint8_t)halfmove;
+            m[4] = (uint8_t)rep; m[5] = 0; m[6] = 0; m[7] = 0;
+            float r0 = 0.0f, r1 = 0.0f;
+            if (!truncated && (rr0 != 0.0f || rr1 != 0.0f)) {
+                r0 = p2r0 == 0 ? rr0 : rr1;
+                r1 = p2r1 == 0 ? rr0 : rr1;
+            }
+            p.out.rewards[2 * b] = r0; p.out.rewards[2 * b + 1] = r1;
+            p.out.terminated[b] = terminal; p.out.truncated[b] = truncated;
+            p.out.step_count[b] = step;
+            p.out.current_player[b] = p2r0 == stm ? 0 : 1;
+            p.out.player_to_role[2 * b] = p2r0; p.out.player_to_role[2 * b + 1] = p2r1;
+        }
+        __syncwarp();
+    }
+}
+
+// observe(state, player) for an explicit role: rebuild from board + history.
+__global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n) {
+    // Simple (non-hot) path: one thread per output float.
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * NF) return;
+    int64_t b = idx / NF;
+    int f = (int)(idx - b * NF);
+    int v = f / 119, kpl = f - 119 * v;
+    const int side = role[b], fl = side ? 56 : 0, sabs = v ^ fl;
+    const int step = step_count[b];
+    const uint8_t* m = st.misc + b * 8;
+    const int castle = m[1], halfmove = m[3];
+    const uint8_t* hist = st.hist + b * (int64_t)HIST_BYTES;
+    const uint32_t* hmeta = reinterpret_cast<const uint32_t*>(hist + RING * 32);
+    float val = 0.0f;
+    if (kpl < 112) {
+        int t = kpl / 14, j = kpl - 14 * t;
+        if (step - t >= 0) {
+            int ply = (step - t) & (RING - 1);
+            uint8_t byte = hist[ply * 32 + (sabs >> 1)];
+            uint8_t pc = (sabs & 1) ? byte >> 4 : byte & 15;
+            int rp = (int)(hmeta[ply] >> 24);
+            if (j < 12) val = (pc && ((color(pc) == side ? 0 : 6) + type(pc) - 1) == j) ? 1.0f : 0.0f;
+            else val = rp >= j - 11 ? 1.0f : 0.0f;
+        }
+    } else if (kpl == 112) val = (float)side;
+    else if (kpl == 113) val = (float)step / 512.0f;
+    else if (kpl == 118) val = (float)halfmove / 100.0f;
+    else {
+        const int own_k = side ? 4 : 1, own_q = side ? 8 : 2, opp_k = side ? 1 : 4, opp_q = side ? 2 : 8;
+        int bit = kpl == 114 ? own_k : kpl == 115 ? own_q : kpl == 116 ? opp_k : opp_q;
+        val = (castle & bit) ? 1.0f : 0.0f;
+    }
+    obs[idx] = val;
+}
+
+static int launch(const Params& p, cudaStream_t s) {
+    int64_t grid = (p.n + kWarps - 1) / kWarps;
+    if (grid > 148 * 12) grid = 148 * 12;
+    step_kernel<<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, 0, s>>>(p);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace chess
+
+extern "C" {
+
+int bbk_chess_init(const bbk_cols* out, const bbk_chess_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
+                   const uint64_t* slot_keys, int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    chess::Params p{};
+    p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.force_reset = 1;
+    return chess::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_chess_step(const bbk_cols* in, const bbk_chess_state* in_s, const bbk_cols* out, const bbk_chess_state* out_s,
+                   const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                   int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    chess::Params p{};
+    p.in = *in; p.in_s = *in_s; p.out = *out; p.out_s = *out_s; p.actions = actions; p.slot_keys = slot_keys;
+    p.n = n; p.slot0 = slot0; p.key = key_state; p.max_steps = max_steps; p.force_reset = 0;
+    return chess::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_chess_observe(const bbk_chess_state* s, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n,
+                      void* stream) {
+    if (n <= 0) return 0;
+    int64_t tot = n * (int64_t)chess::NF;
+    chess::observe_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*s, step_count, role, obs, n);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

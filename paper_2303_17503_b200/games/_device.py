@@ -31,6 +31,46 @@ def _torch():
     return torch
 
 
+_UID = [0]
+
+
+def _next_uid() -> int:
+    _UID[0] += 1
+    return _UID[0]
+
+
+class Lineage:
+    """Which batches of a trajectory may still be stepped.
+
+    Games with an in-place per-env history (Go superko store, chess/shogi
+    repetition rings) share it along a trajectory. ``head`` is the newest
+    batch; ``trail`` its predecessors (newest first). Stepping the head is
+    the fast path; stepping a recent predecessor is a branch (the game
+    decides whether that needs a private copy); anything older raises
+    StaleBatch.
+    """
+
+    def __init__(self, uid: int):
+        self.head = uid
+        self.trail: list[int] = []
+
+    def depth(self, uid: int) -> int:
+        if uid == self.head:
+            return 0
+        try:
+            return self.trail.index(uid) + 1
+        except ValueError:
+            return 1 << 30
+
+    def advance(self, parent: int, child: int, keep: int = 2) -> None:
+        if parent == self.head:
+            self.trail = ([parent] + self.trail)[:keep]
+        else:   # branch: the old head (and anything newer than parent) is dropped
+            i = self.trail.index(parent)
+            self.trail = self.trail[i:i + keep]
+        self.head = child
+
+
 class DeviceV:
     """Struct-of-arrays device state of one batch (reference V, tictactoe.py:74-79)."""
 
@@ -47,7 +87,7 @@ class DeviceV:
         self.dev = SimpleNamespace()
         self.priv = SimpleNamespace()
         self.store = None
-        self.gen = 0
+        self.uid = _next_uid()
         self._host = {}
 
     # lazily materialised host columns (the reference reads them via getattr)
@@ -177,15 +217,15 @@ class DeviceKernel:
         else:
             out.t = v.t + 1
             out.limit = limit
+            out.uid = _next_uid()
             out._host = {}
         self.prepare_step(v, out)
         self.launch_step(v, out, a, ks, sk, limit)
         return out
 
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
-        """Hook for games with shared append-only stores (Go)."""
+        """Hook for games with shared in-place stores (Go, chess, shogi)."""
         out.store = v.store
-        out.gen = v.gen + 1
 
     # ----------------------------------------------------- protocol: state_at
     def host_snapshot(self, v: DeviceV) -> dict:

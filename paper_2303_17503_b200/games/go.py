@@ -21,7 +21,7 @@ import numpy as np
 
 from .. import _native as nat
 from ..core import GameDef, GameSpec, StaleBatch, UnsupportedGame
-from ._device import DeviceKernel, DeviceV, _torch
+from ._device import DeviceKernel, DeviceV, Lineage, _torch
 
 HISTORY_PLANES = 8
 
@@ -64,7 +64,7 @@ class GoStore:
         self.history = history
         self.bloom = bloom
         self.hist_cap = hist_cap
-        self.head = 0
+        self.lineage = None
 
     def struct(self) -> nat.GoStore:
         return nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
@@ -107,8 +107,7 @@ class GoKernel(DeviceKernel):
 
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
         v.store = self.new_store(v.n, v.limit, v.device)
-        v.gen = 0
-        v.store.head = 0
+        v.store.lineage = Lineage(v.uid)
         cols, st, store = self.cols(v), self.state_struct(v), v.store.struct()
         nat.check(nat.lib().bbk_go_init(self.size, cols, st, store, v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_go_init")
@@ -117,18 +116,19 @@ class GoKernel(DeviceKernel):
         store = v.store
         if out.limit + 2 > store.hist_cap:
             raise ValueError("max_steps exceeds the history capacity of this batch")
-        if v.gen != store.head:
-            if store.head - v.gen > 2:
-                raise StaleBatch(f"batch is {store.head - v.gen} steps behind its lineage; only the last two "
-                                 "predecessors can be stepped again")
-            # branch: private copy of the history, filters rebuilt for v's lengths
+        depth = store.lineage.depth(v.uid)
+        if depth > 2:
+            raise StaleBatch("batch is too far behind its lineage; only the last two predecessors of the "
+                             "newest batch can be stepped again")
+        if depth > 0:
+            # branch: private copy of the history, filters rebuilt for v's lengths; the
+            # original lineage keeps its store
             store = GoStore(store.history.clone(), store.bloom.clone(), store.hist_cap)
-            store.head = v.gen
+            store.lineage = Lineage(v.uid)
             nat.check(nat.lib().bbk_go_rebuild_bloom(store.struct(), nat.ptr(v.priv.hist_len), v.n,
                                                      nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
         out.store = store
-        out.gen = v.gen + 1
-        store.head = out.gen
+        store.lineage.advance(v.uid, out.uid)
 
     def launch_step(self, v, out, a, ks, sk, limit) -> None:
         nat.check(nat.lib().bbk_go_step(self.size, self.komi, self.cols(v), self.state_struct(v), self.cols(out),
@@ -147,10 +147,10 @@ class GoKernel(DeviceKernel):
     def slice_store(self, v: DeviceV, w: DeviceV, i: int) -> None:
         s = v.store
         w.store = GoStore(s.history[i:i + 1].clone(), s.bloom[i:i + 1].clone(), s.hist_cap)
-        w.gen = 0
-        w.store.head = 0
-        if v.gen != s.head:
-            if s.head - v.gen > 2:
+        w.store.lineage = Lineage(w.uid)
+        depth = s.lineage.depth(v.uid)
+        if depth > 0:
+            if depth > 2:
                 raise StaleBatch("batch too far behind its lineage to slice")
             nat.check(nat.lib().bbk_go_rebuild_bloom(w.store.struct(), nat.ptr(w.priv.hist_len), 1,
                                                      nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
