@@ -130,6 +130,28 @@ int bbk_chess_step(const bbk_cols* in, const bbk_chess_state* in_s, const bbk_co
 int bbk_chess_observe(const bbk_chess_state* s, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n,
                       void* stream);
 
+/* --------------------------------------------------------------- Shogi --
+ * No reference engine (reserved spec, games/__init__.py:31); rules and
+ * encodings per PAPER.md:1278-1354 and DESIGN.md §3.4 (CPU twin:
+ * oracle/orc_shogi.c, perft-pinned).
+ *   board[n, 96]  absolute piece codes (owner << 4 | FU1 KY2 KE3 GI4 KI5 KA6 HI7 OU8 TO..RY 9-14), 81 used
+ *   misc[n, 16]   hands[2][7] (FU KY KE GI KI KA HI), side to move, repetition count
+ *   hist[n, hist_cap] u64 position keys by ply (four-fold repetition), shared in place. */
+typedef struct bbk_shogi_state {
+    uint8_t*  board;
+    uint8_t*  misc;
+    uint64_t* hist;
+    int32_t   hist_cap;
+} bbk_shogi_state;
+
+int bbk_shogi_init(const bbk_cols* out, const bbk_shogi_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
+                   const uint64_t* slot_keys, int32_t max_steps, void* stream);
+int bbk_shogi_step(const bbk_cols* in, const bbk_shogi_state* in_s, const bbk_cols* out, const bbk_shogi_state* out_s,
+                   const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                   int32_t max_steps, void* stream);
+int bbk_shogi_observe(const bbk_shogi_state* s, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n,
+                      void* stream);
+
 /* ------------------------------------------------------------- generic --
  * agents.random_actions (agents.py:33-46): a_i = index of the d-th legal
  * action, d = child(key, slot0+i) % max(popcount(mask_i), 1); 0 if none. */

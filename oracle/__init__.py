@@ -73,6 +73,8 @@ def lib():
             L.orc_shogi_new.restype = _P
             L.orc_shogi_perft.argtypes = [C.c_char_p, C.c_int]
             L.orc_shogi_perft.restype = C.c_uint64
+            L.orc_shogi_set_sfen.argtypes = [_P, _I64, C.c_char_p]
+            L.orc_shogi_set_sfen.restype = C.c_int
         if hasattr(L, "omp_set_num_threads"):
             pass
         _LIB = L
@@ -277,6 +279,13 @@ class ShogiBatch(_Batch):
 
     def __init__(self, n: int, max_steps: int = 256):
         super().__init__(lib().orc_shogi_new(n, max_steps), n)
+
+    def set_sfen(self, i: int, sfen: str):
+        assert self.L.orc_shogi_set_sfen(self.h, i, sfen.encode()) == 0
+
+    @staticmethod
+    def perft(sfen, depth: int) -> int:
+        return int(lib().orc_shogi_perft(None if sfen is None else sfen.encode(), depth))
 
 
 class Session:

@@ -54,7 +54,7 @@ class ChessState(C.Structure):
 
 
 class ShogiState(C.Structure):
-    _fields_ = [("board", P), ("misc", P), ("hist", P)]
+    _fields_ = [("board", P), ("misc", P), ("hist", P), ("hist_cap", I32)]
 
 
 def _declare(L):

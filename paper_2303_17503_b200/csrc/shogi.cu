@@ -1,0 +1,642 @@
+// Shogi batched step for sm_100a (no reference engine: PAPER.md:1278-1354 +
+// DESIGN.md §3.4 conventions; CPU twin oracle/orc_shogi.c, perft-pinned).
+//
+// One warp per board. After lane 0 applies the action, the board is copied
+// into shared memory in the MOVER'S FRAME with owner-relative colours (own
+// pieces move "up"), so every rule below is side-agnostic:
+//   * attack gather: for each target square, walk the 8 rays and the 4 knight
+//     squares once and record (for both owners) the 14-bit mask of attacking
+//     piece types and the attacker count -> the observation's attack planes,
+//     the in-check plane and the checkers;
+//   * legal moves: rays out of the own king give checkers, block squares and
+//     pins; lanes own squares and emit step / slide / knight moves (promotion
+//     choices, dead-piece rule), king moves against a king-transparent attack
+//     test, and drops (nifu, dead squares, check blocks); a pawn drop in front
+//     of the enemy king runs a warp-parallel mate test (uchifuzume);
+//   * four-fold repetition through 64-bit position keys (scan of the ply log);
+//   * observation: a 9639-bit stream (one bit per float, every plane is
+//     binary) emitted as float4 through a LUT into the flat [n, 9, 9, 119]
+//     stream (records are not 16-B aligned, edges use scalar stores).
+#include "common.cuh"
+#include "../../include/bbk.h"
+
+namespace shogi {
+using namespace bbk;
+
+constexpr int A = 2187;
+constexpr int NF = 81 * 119;        // 9639 floats per record
+constexpr int kWarps = 4;
+constexpr int BOARD_STRIDE = 96;
+constexpr int MISC = 16;            // hand[2][7], stm, rep
+
+enum { EMP = 0, FU = 1, KY, KE, GI, KI, KA, HI, OU, TO, NY, NK, NG, UM, RY };
+
+// direction index d: 0 UP(-1,0) 1 UP_LEFT(-1,-1) 2 UP_RIGHT(-1,+1) 3 LEFT(0,-1)
+// 4 RIGHT(0,+1) 5 DOWN(+1,0) 6 DOWN_LEFT(+1,-1) 7 DOWN_RIGHT(+1,+1)
+__device__ __constant__ int8_t DR[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+__device__ __constant__ int8_t DC[8] = {0, -1, 1, -1, 1, 0, -1, 1};
+__device__ __constant__ int8_t OPPD[8] = {5, 7, 6, 4, 3, 0, 2, 1};
+// per type (index = type): step directions and slide directions (owner frame)
+__device__ __constant__ uint8_t STEP[16] = {0, 0x01, 0x00, 0x00, 0xC7, 0x3F, 0x00, 0x00, 0xFF, 0x3F, 0x3F, 0x3F, 0x3F,
+                                            0x39, 0xC6, 0};
+__device__ __constant__ uint8_t SLIDE[16] = {0, 0x00, 0x01, 0x00, 0x00, 0x00, 0xC6, 0x39, 0x00, 0, 0, 0, 0, 0xC6, 0x39, 0};
+__device__ __constant__ uint8_t HAND_TYPE[7] = {FU, KY, KE, GI, KI, KA, HI};
+__device__ __constant__ uint8_t HCAP[7] = {8, 4, 4, 4, 4, 2, 2};
+__device__ __constant__ uint8_t HOFF[7] = {0, 8, 12, 16, 20, 24, 26};
+
+struct WarpSmem {
+    alignas(16) uint8_t mask[A + 48];
+    alignas(16) uint32_t bits[NF / 32 + 4];
+    uint8_t bd[96];            // mover frame, owner-relative: (owner << 4) | type, owner 0 = side to move
+    uint8_t abs_[96];          // absolute board (state)
+    uint16_t atk[2][81];       // attacking piece-type masks per owner
+    uint8_t acnt[2][81];
+    uint8_t kesc[8];           // own king: neighbour d is a legal king destination
+    uint64_t pinray[8][2];     // 81-bit ray masks (lo 64 | hi 17)
+    int8_t pinsq[8];
+};
+
+struct Params {
+    bbk_cols in, out;
+    bbk_shogi_state in_s, out_s;
+    const int64_t* actions;
+    const uint64_t* slot_keys;
+    int64_t n, slot0;
+    uint64_t key;
+    int32_t max_steps;
+    int force_reset;
+};
+
+struct M81 {   // 81-bit square set
+    uint64_t lo, hi;
+    __device__ __forceinline__ bool has(int s) const { return s < 64 ? (lo >> s) & 1ull : (hi >> (s - 64)) & 1ull; }
+    __device__ __forceinline__ void set(int s) { if (s < 64) lo |= 1ull << s; else hi |= 1ull << (s - 64); }
+};
+
+__device__ __forceinline__ bool son(int r, int c) { return (unsigned)r < 9u && (unsigned)c < 9u; }
+__device__ __forceinline__ int owner(uint8_t pc) { return pc >> 4; }
+__device__ __forceinline__ int ptype(uint8_t pc) { return pc & 15; }
+__device__ __forceinline__ bool promotable(int t) { return t == FU || t == KY || t == KE || t == GI || t == KA || t == HI; }
+__device__ __forceinline__ int promote(int t) { return t <= GI ? t + 8 : t == KA ? UM : RY; }
+__device__ __forceinline__ int unpromote(int t) { return (t >= TO && t <= NG) ? t - 8 : t == UM ? KA : t == RY ? HI : t; }
+
+// Board accessor with up to three overridden squares (scratch positions).
+struct Acc {
+    const uint8_t* bd;
+    int s0, s1, s2;
+    uint8_t v0, v1, v2;
+    __device__ __forceinline__ uint8_t operator()(int s) const {
+        return s == s0 ? v0 : s == s1 ? v1 : s == s2 ? v2 : bd[s];
+    }
+};
+
+// Does side w (0 = mover, 1 = opponent; owner-relative codes) attack square t?
+__device__ bool attacked(const Acc& at, int t, int w) {
+    const int r = t / 9, c = t - 9 * (t / 9);
+    for (int d = 0; d < 8; d++) {
+        int rr = r + DR[d], cc = c + DC[d], k = 1;
+        while (son(rr, cc)) {
+            uint8_t pc = at(rr * 9 + cc);
+            if (pc) {
+                if (owner(pc) == w) {
+                    const int ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
+                    if (((k == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) return true;
+                }
+                break;
+            }
+            rr += DR[d]; cc += DC[d]; k++;
+        }
+    }
+    const int kr = w == 0 ? r + 2 : r - 2;   // knights: own move (-2, +-1), opponent (+2, +-1)
+    for (int dc = -1; dc <= 1; dc += 2)
+        if (son(kr, c + dc)) { uint8_t pc = at(kr * 9 + c + dc); if (pc && owner(pc) == w && ptype(pc) == KE) return true; }
+    return false;
+}
+
+__device__ __forceinline__ int action_code(int dir, bool promo, int to) { return (dir + (promo ? 10 : 0)) * 81 + to; }
+
+// ---------------------------------------------------------------- apply
+// Apply the action (mover frame of `stm`) to the absolute board + hands. Lane 0.
+__device__ void apply_action(uint8_t* abs_, uint8_t* hand /* [2][7] */, int stm, int a) {
+    const int dir = a / 81, to = a - 81 * dir;
+    auto fr = [&](int s) { return stm ? 80 - s : s; };
+    const int tabs = fr(to);
+    if (dir >= 20) {
+        const int hi = dir - 20;
+        hand[stm * 7 + hi] -= 1;
+        abs_[tabs] = (uint8_t)((stm << 4) | HAND_TYPE[hi]);
+        return;
+    }
+    const bool promo = dir >= 10;
+    const int d = dir % 10;
+    const int tr = to / 9, tc = to - 9 * (to / 9);
+    int from;
+    if (d >= 8) {
+        from = (tr + 2) * 9 + tc + (d == 8 ? 1 : -1);   // knight came from (+2, -+1)
+    } else {
+        int rr = tr - DR[d], cc = tc - DC[d];
+        from = rr * 9 + cc;
+        while (!abs_[fr(from)]) { rr -= DR[d]; cc -= DC[d]; from = rr * 9 + cc; }
+    }
+    const int fabs = fr(from);
+    const uint8_t pc = abs_[fabs], cap = abs_[tabs];
+    if (cap) {
+        int ct = unpromote(cap & 15);
+        hand[stm * 7 + ct - 1] += 1;
+    }
+    abs_[tabs] = promo ? (uint8_t)((stm << 4) | promote(pc & 15)) : pc;
+    abs_[fabs] = EMP;
+}
+
+__device__ __forceinline__ uint64_t sq_key(uint8_t pc, int s) {
+    return mix64(0x5306100000000000ULL + (uint64_t)pc * 128 + (uint64_t)s);
+}
+
+// Attack gather: for every target square, the piece types (14-bit mask) and
+// number of pieces of each owner attacking it (obs planes 14-30 / 45-61).
+__device__ void gather_attacks(WarpSmem& S, int lane) {
+    const uint8_t* bd = S.bd;
+    for (int t = lane; t < 81; t += 32) {
+        const int r = t / 9, c = t - 9 * r;
+        uint16_t m0 = 0, m1 = 0;
+        uint8_t n0 = 0, n1 = 0;
+        for (int d = 0; d < 8; d++) {
+            int rr = r + DR[d], cc = c + DC[d], kk = 1;
+            while (son(rr, cc)) {
+                uint8_t pc = bd[rr * 9 + cc];
+                if (pc) {
+                    const int w = owner(pc), ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
+                    if (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) {
+                        if (w == 0) { m0 |= 1u << (ty - 1); n0++; } else { m1 |= 1u << (ty - 1); n1++; }
+                    }
+                    break;
+                }
+                rr += DR[d]; cc += DC[d]; kk++;
+            }
+        }
+        for (int dc = -1; dc <= 1; dc += 2) {
+            if (son(r + 2, c + dc) && bd[(r + 2) * 9 + c + dc] == KE) { m0 |= 1u << (KE - 1); n0++; }
+            if (son(r - 2, c + dc) && bd[(r - 2) * 9 + c + dc] == (16 | KE)) { m1 |= 1u << (KE - 1); n1++; }
+        }
+        S.atk[0][t] = m0; S.atk[1][t] = m1; S.acnt[0][t] = n0; S.acnt[1][t] = n1;
+    }
+}
+
+// Observation: 9639-bit stream (bit f = float f of the record) then float4 emission.
+__device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t* hand, int side, bool in_check,
+                                   float* obs_stream, int64_t b, int lane) {
+    const uint8_t* bd = S.bd;
+    // ---- observation bitstream
+    for (int i = lane; i < NF / 32 + 4; i += 32) S.bits[i] = 0u;
+    __syncwarp();
+    uint32_t cpat[4] = {0u, 0u, 0u, 0u};   // constant planes 62..118 (hands, check)
+    {
+        for (int who = 0; who < 2; who++) {
+            const int own_side = who == 0 ? side : 1 - side;
+            for (int hi = 0; hi < 7; hi++) {
+                const int cntp = hand[own_side * 7 + hi] < HCAP[hi] ? hand[own_side * 7 + hi] : HCAP[hi];
+                for (int q = 0; q < cntp; q++) {
+                    const int bit = 62 + 28 * who + HOFF[hi] + q;
+                    cpat[bit >> 5] |= 1u << (bit & 31);
+                }
+            }
+        }
+        if (in_check) cpat[118 >> 5] |= 1u << (118 & 31);
+    }
+    for (int pass = 0; pass < 4; pass++) {
+        const int s = pass < 2 ? 2 * lane + pass : 64 + 2 * lane + (pass - 2);
+        if (s < 81) {
+            uint32_t w[4] = {cpat[0], cpat[1], cpat[2], cpat[3]};
+            const uint8_t pc = bd[s];
+            if (pc) {
+                const int bit = 31 * owner(pc) + ptype(pc) - 1;
+                w[bit >> 5] |= 1u << (bit & 31);
+            }
+#pragma unroll
+            for (int who = 0; who < 2; who++) {
+                const uint32_t am = S.atk[who][s];
+                const int base = 31 * who + 14;
+                // 14 type bits at [base, base+14)
+                const uint64_t v = (uint64_t)am << (base & 31);
+                w[base >> 5] |= (uint32_t)v;
+                if ((base >> 5) + 1 < 4) w[(base >> 5) + 1] |= (uint32_t)(v >> 32);
+                const int n = S.acnt[who][s];
+                for (int q = 0; q < 3; q++)
+                    if (n > q) { const int bit = base + 14 + q; w[bit >> 5] |= 1u << (bit & 31); }
+            }
+            const int off = 119 * s, wi = off >> 5, sh = off & 31;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                S.bits[wi + j] |= w[j] << sh;
+                if (sh) S.bits[wi + j + 1] |= w[j] >> (32 - sh);
+            }
+        }
+        __syncwarp();
+    }
+    if (obs_stream) {
+        float* obs = obs_stream;
+        const int64_t F0 = b * (int64_t)NF;
+        const int64_t a0 = (F0 + 3) & ~(int64_t)3, a1 = (F0 + NF) & ~(int64_t)3;
+        if (lane < 8) {
+            const int64_t f = lane < 4 ? F0 + lane : a1 + (lane - 4);
+            const bool ok = lane < 4 ? f < a0 : f < F0 + NF;
+            if (ok) {
+                const uint32_t fi = (uint32_t)(f - F0);
+                obs[f] = (float)((S.bits[fi >> 5] >> (fi & 31)) & 1u);
+            }
+        }
+        float4* o4 = reinterpret_cast<float4*>(obs);
+        for (int64_t j = (a0 >> 2) + lane; j < (a1 >> 2); j += 32) {
+            const uint32_t fi = (uint32_t)((j << 2) - F0);
+            const uint64_t w2 = (uint64_t)S.bits[fi >> 5] | ((uint64_t)S.bits[(fi >> 5) + 1] << 32);
+            o4[j] = lut[(uint32_t)(w2 >> (fi & 31)) & 15u];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
+    __shared__ WarpSmem sm[kWarps];
+    __shared__ float4 lut[16];
+    if (threadIdx.x < 16) {
+        uint32_t q = threadIdx.x;
+        lut[q] = make_float4((float)(q & 1), (float)((q >> 1) & 1), (float)((q >> 2) & 1), (float)((q >> 3) & 1));
+    }
+    __syncthreads();
+    WarpSmem& S = sm[threadIdx.x >> 5];
+    const int lane = lane_id();
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    const int cap = p.out_s.hist_cap;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
+        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+        const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
+        uint64_t* hist = p.out_s.hist + b * (int64_t)cap;
+        int8_t p2r0, p2r1;
+        int stm, step;
+        uint8_t hand[14];
+        if (reset) {
+            int c = (int)(child(k, 0) % 2ull);
+            p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
+            // lnsgkgsnl/1r5b1/ppppppppp/9/9/9/PPPPPPPPP/1B5R1/LNSGKGSNL (White = owner 1 at the top)
+            const uint8_t back[9] = {KY, KE, GI, KI, OU, KI, GI, KE, KY};
+            for (int s = lane; s < 96; s += 32) {
+                uint8_t v = 0;
+                if (s < 81) {
+                    int r = s / 9, cc = s - 9 * r;
+                    if (r == 0) v = (uint8_t)(16 | back[cc]);
+                    else if (r == 1) v = cc == 1 ? (uint8_t)(16 | HI) : cc == 7 ? (uint8_t)(16 | KA) : 0;
+                    else if (r == 2) v = 16 | FU;
+                    else if (r == 6) v = FU;
+                    else if (r == 7) v = cc == 1 ? KA : cc == 7 ? HI : 0;
+                    else if (r == 8) v = back[cc];
+                }
+                S.abs_[s] = v;
+            }
+#pragma unroll
+            for (int j = 0; j < 14; j++) hand[j] = 0;
+            stm = 0; step = 0;
+            __syncwarp();
+        } else {
+            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
+            const uint8_t* ib = p.in_s.board + b * BOARD_STRIDE;
+            for (int s = lane; s < 96; s += 32) S.abs_[s] = ib[s];
+            const uint8_t* m = p.in_s.misc + b * MISC;
+#pragma unroll
+            for (int j = 0; j < 14; j++) hand[j] = m[j];
+            stm = m[14];
+            step = p.in.step_count[b] + 1;
+            __syncwarp();
+            if (lane == 0) apply_action(S.abs_, hand, stm, (int)p.actions[b]);
+#pragma unroll
+            for (int j = 0; j < 14; j++) hand[j] = (uint8_t)__shfl_sync(BBK_FULL, (int)hand[j], 0);
+            stm ^= 1;
+            __syncwarp();
+        }
+        const int side = stm;
+        // mover-frame, owner-relative board
+        for (int s = lane; s < 81; s += 32) {
+            uint8_t v = S.abs_[side ? 80 - s : s];
+            S.bd[s] = v ? (uint8_t)((((v >> 4) ^ side) << 4) | (v & 15)) : (uint8_t)0;
+        }
+        for (int i = lane; i < (A + 48) / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        const uint8_t* bd = S.bd;
+        const int64_t mstart = b * (int64_t)A;
+        uint8_t* mk = S.mask + (mstart & 15);   // mask byte i staged at the destination's 16-byte phase
+        // ---- king squares, attack gather (both owners), pawn columns
+        int ksq = -1, oksq = -1;
+        uint32_t pawncols = 0u;
+        for (int s = lane; s < 81; s += 32) {
+            uint8_t pc = bd[s];
+            if (pc == OU) ksq = s;
+            if (pc == (16 | OU)) oksq = s;
+            if (pc == FU) pawncols |= 1u << (s % 9);
+        }
+        {
+            unsigned bk = __ballot_sync(BBK_FULL, ksq >= 0), bo = __ballot_sync(BBK_FULL, oksq >= 0);
+            ksq = __shfl_sync(BBK_FULL, ksq, bk ? __ffs(bk) - 1 : 0);
+            oksq = __shfl_sync(BBK_FULL, oksq, bo ? __ffs(bo) - 1 : 0);
+            pawncols = __reduce_or_sync(BBK_FULL, pawncols);
+        }
+        gather_attacks(S, lane);
+        __syncwarp();
+        const bool in_check = ksq >= 0 && S.acnt[1][ksq] > 0;
+        // ---- checkers / block squares / pins along the 8 rays out of the king
+        bool checker = false;
+        M81 block{0ull, 0ull};
+        const int kr = ksq / 9, kc = ksq - 9 * (ksq / 9);
+        if (lane < 8) {
+            const int d = lane;
+            int rr = kr + DR[d], cc = kc + DC[d], kk = 1, own = -1;
+            M81 ray{0ull, 0ull};
+            int8_t pin = -1;
+            M81 pray{0ull, 0ull};
+            while (son(rr, cc)) {
+                const int s = rr * 9 + cc;
+                ray.set(s);
+                const uint8_t pc = bd[s];
+                if (pc) {
+                    const int ty = ptype(pc);
+                    if (own < 0) {
+                        if (owner(pc) == 0) own = s;
+                        else {
+                            if (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> d) & 1) { checker = true; block = ray; }
+                            break;
+                        }
+                    } else {
+                        if (owner(pc) == 1 && ((SLIDE[ty] >> d) & 1)) { pin = (int8_t)own; pray = ray; }
+                        break;
+                    }
+                }
+                rr += DR[d]; cc += DC[d]; kk++;
+            }
+            S.pinsq[d] = pin;
+            S.pinray[d][0] = pray.lo; S.pinray[d][1] = pray.hi;
+            // king destination d: on board, not own, not attacked with the king lifted
+            const int tr = kr + DR[d], tc = kc + DC[d];
+            bool ok = false;
+            if (son(tr, tc)) {
+                const int t = tr * 9 + tc;
+                const uint8_t q = bd[t];
+                if (!(q && owner(q) == 0)) {
+                    Acc at{bd, ksq, t, -1, 0, OU, 0};
+                    ok = !attacked(at, t, 1);
+                }
+            }
+            S.kesc[d] = ok;
+        } else if (lane < 10) {   // knight checkers: opponent knights at (kr-2, kc-+1)
+            const int cc = kc + (lane == 8 ? -1 : 1), rr = kr - 2;
+            if (son(rr, cc) && bd[rr * 9 + cc] == (16 | KE)) { checker = true; block.set(rr * 9 + cc); }
+        }
+        const int nchecks = __popc(__ballot_sync(BBK_FULL, checker));
+        M81 chk;
+        chk.lo = ((uint64_t)__reduce_or_sync(BBK_FULL, (uint32_t)(block.lo >> 32)) << 32) |
+                 __reduce_or_sync(BBK_FULL, (uint32_t)block.lo);
+        chk.hi = __reduce_or_sync(BBK_FULL, (uint32_t)block.hi);
+        if (nchecks == 0) { chk.lo = ~0ull; chk.hi = ~0ull; }
+        else if (nchecks >= 2) { chk.lo = 0ull; chk.hi = 0ull; }
+        __syncwarp();
+        // ---- moves of own pieces (lanes own squares)
+        int cnt = 0;
+        for (int s = lane; s < 81; s += 32) {
+            const uint8_t pc = bd[s];
+            if (!pc || owner(pc) != 0) continue;
+            const int ty = ptype(pc), r = s / 9, c = s - 9 * r;
+            if (ty == OU) {
+                for (int d = 0; d < 8; d++)
+                    if (S.kesc[d]) { mk[action_code(d, false, s + DR[d] * 9 + DC[d])] = 1; cnt++; }
+                continue;
+            }
+            M81 allow = chk;
+#pragma unroll
+            for (int d = 0; d < 8; d++)
+                if (S.pinsq[d] == s) { allow.lo &= S.pinray[d][0]; allow.hi &= S.pinray[d][1]; }
+            auto emit = [&](int d, int to) {
+                if (!allow.has(to)) return;
+                const int trow = to / 9;
+                const bool can_promo = promotable(ty) && (r <= 2 || trow <= 2);
+                const bool must = (ty == FU || ty == KY) ? trow == 0 : ty == KE ? trow <= 1 : false;
+                if (can_promo) { mk[action_code(d, true, to)] = 1; cnt++; }
+                if (!must) { mk[action_code(d, false, to)] = 1; cnt++; }
+            };
+            if (ty == KE) {
+                for (int j = 0; j < 2; j++) {
+                    const int rr = r - 2, cc = c + (j ? 1 : -1);
+                    if (!son(rr, cc)) continue;
+                    const uint8_t q = bd[rr * 9 + cc];
+                    if (q && owner(q) == 0) continue;
+                    emit(8 + j, rr * 9 + cc);
+                }
+                continue;
+            }
+            const uint8_t st = STEP[ty], sl = SLIDE[ty];
+            for (int d = 0; d < 8; d++) {
+                if (!(((st | sl) >> d) & 1)) continue;
+                int rr = r + DR[d], cc = c + DC[d];
+                const bool slide = (sl >> d) & 1;
+                while (son(rr, cc)) {
+                    const int to = rr * 9 + cc;
+                    const uint8_t q = bd[to];
+                    if (q && owner(q) == 0) break;
+                    emit(d, to);
+                    if (q || !slide) break;
+                    rr += DR[d]; cc += DC[d];
+                }
+            }
+        }
+        // ---- drops (block squares only when in single check; none in double check)
+        const M81 dropok = chk;   // the checker's own square is occupied, so drops only block
+        const int my = side * 7;
+        for (int s = lane; s < 81; s += 32) {
+            if (bd[s]) continue;
+            if (nchecks >= 2) continue;
+            if (nchecks == 1 && !dropok.has(s)) continue;
+            const int r = s / 9, c = s - 9 * r;
+            for (int hi = 0; hi < 7; hi++) {
+                if (!hand[my + hi]) continue;
+                const int ty = HAND_TYPE[hi];
+                if ((ty == FU || ty == KY) && r == 0) continue;
+                if (ty == KE && r <= 1) continue;
+                if (ty == FU) {
+                    if ((pawncols >> c) & 1u) continue;
+                    if (oksq >= 0 && s == oksq + 9) continue;   // uchifuzume candidate: decided below
+                }
+                mk[action_code(20 + hi, false, s)] = 1;
+                cnt++;
+            }
+        }
+        // uchifuzume: pawn drop on the square in front of the enemy king
+        {
+            const int D = oksq + 9;
+            bool cand = oksq >= 0 && oksq + 9 < 81 && hand[my + 0] && !bd[D] && !((pawncols >> (D % 9)) & 1u) &&
+                        nchecks < 2 && (nchecks == 0 || chk.has(D));
+            if (cand) {
+                // after the drop: can the enemy king escape, or can an enemy piece take the pawn?
+                bool reply = false;
+                const int okr = oksq / 9, okc = oksq - 9 * okr;
+                if (lane < 8) {
+                    const int tr = okr + DR[lane], tc = okc + DC[lane];
+                    if (son(tr, tc)) {
+                        const int t = tr * 9 + tc;
+                        const uint8_t q = t == D ? (uint8_t)FU : bd[t];
+                        if (!(q && owner(q) == 1)) {
+                            Acc at{bd, D, oksq, t, (uint8_t)FU, 0, (uint8_t)(16 | OU)};
+                            reply = !attacked(at, t, 0);
+                        }
+                    }
+                } else if (lane < 18) {   // lanes 8..15: ray attackers of D; 16,17: knights
+                    const int dr_ = D / 9, dc_ = D - 9 * (D / 9);
+                    int from = -1;
+                    if (lane < 16) {
+                        const int d = lane - 8;
+                        int rr = dr_ + DR[d], cc = dc_ + DC[d], kk = 1;
+                        while (son(rr, cc)) {
+                            const uint8_t pc = bd[rr * 9 + cc];
+                            if (pc) {
+                                const int ty = ptype(pc);
+                                if (owner(pc) == 1 && ty != OU && (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> d) & 1))
+                                    from = rr * 9 + cc;
+                                break;
+                            }
+                            rr += DR[d]; cc += DC[d]; kk++;
+                        }
+                    } else {
+                        const int rr = dr_ - 2, cc = dc_ + (lane == 16 ? -1 : 1);
+                        if (son(rr, cc) && bd[rr * 9 + cc] == (16 | KE)) from = rr * 9 + cc;
+                    }
+                    if (from >= 0) {
+                        Acc at{bd, D, from, -1, bd[from], 0, 0};
+                        reply = !attacked(at, oksq, 0);
+                    }
+                }
+                const bool any_reply = __any_sync(BBK_FULL, reply);
+                if (lane == 0 && any_reply) { mk[action_code(20, false, D)] = 1; cnt++; }
+            }
+        }
+        const int nlegal = warp_sum(cnt);
+        // ---- position key + four-fold repetition
+        uint64_t key = 0ull;
+        for (int s = lane; s < 81; s += 32) { uint8_t v = S.abs_[s]; if (v) key ^= sq_key(v, s); }
+        if (lane < 14 && hand[lane]) {
+            const int c = lane / 7, i = lane - 7 * c;
+            key ^= mix64(0x5306200000000000ULL + (uint64_t)(c * 8 + i) * 32 + hand[lane]);
+        }
+        key = warp_xor64(key);
+        if (side) key ^= mix64(0x5306300000000000ULL);
+        int reps = 0;
+        for (int j = lane; j < step; j += 32) reps += hist[j] == key;
+        reps = warp_sum(reps);
+        if (lane == 0) hist[step] = key;
+        bool terminal = false;
+        float rr0 = 0.0f, rr1 = 0.0f;
+        if (nlegal == 0) {   // no legal move: the side to move loses
+            terminal = true;
+            if (side == 0) { rr0 = -1.0f; rr1 = 1.0f; } else { rr0 = 1.0f; rr1 = -1.0f; }
+        } else if (reps >= 3) {
+            terminal = true;
+        }
+        const bool truncated = !terminal && step >= p.max_steps;
+        build_and_emit_obs(S, lut, hand, side, in_check, p.out.observation, b, lane);
+        // ---- mask emission (flat byte stream; records are not 16-B aligned)
+        __syncwarp();
+        if (terminal || truncated)
+            for (int i = lane; i < (A + 48) / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.mask);
+        // ---- state + columns
+        uint8_t* ob = p.out_s.board + b * BOARD_STRIDE;
+        for (int s = lane; s < 96; s += 32) ob[s] = S.abs_[s];
+        const int rep = reps > 3 ? 3 : reps;
+        if (lane == 0) {
+            uint8_t* m = p.out_s.misc + b * MISC;
+            for (int j = 0; j < 14; j++) m[j] = hand[j];
+            m[14] = (uint8_t)side; m[15] = (uint8_t)rep;
+            float r0 = 0.0f, r1 = 0.0f;
+            if (!truncated && (rr0 != 0.0f || rr1 != 0.0f)) { r0 = p2r0 == 0 ? rr0 : rr1; r1 = p2r1 == 0 ? rr0 : rr1; }
+            p.out.rewards[2 * b] = r0; p.out.rewards[2 * b + 1] = r1;
+            p.out.terminated[b] = terminal; p.out.truncated[b] = truncated;
+            p.out.step_count[b] = step;
+            p.out.current_player[b] = p2r0 == side ? 0 : 1;
+            p.out.player_to_role[2 * b] = p2r0; p.out.player_to_role[2 * b + 1] = p2r1;
+        }
+        __syncwarp();
+    }
+}
+
+
+// observe(state, player) for an explicit role per slot (no history planes in shogi).
+__global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st, const uint8_t* role, float* obs,
+                                                              int64_t n) {
+    __shared__ WarpSmem sm[kWarps];
+    __shared__ float4 lut[16];
+    if (threadIdx.x < 16) {
+        uint32_t q = threadIdx.x;
+        lut[q] = make_float4((float)(q & 1), (float)((q >> 1) & 1), (float)((q >> 2) & 1), (float)((q >> 3) & 1));
+    }
+    __syncthreads();
+    WarpSmem& S = sm[threadIdx.x >> 5];
+    const int lane = lane_id();
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < n; b += nwarps) {
+        const int side = role[b];
+        const uint8_t* ib = st.board + b * BOARD_STRIDE;
+        for (int s = lane; s < 81; s += 32) {
+            uint8_t v = ib[side ? 80 - s : s];
+            S.bd[s] = v ? (uint8_t)((((v >> 4) ^ side) << 4) | (v & 15)) : (uint8_t)0;
+        }
+        uint8_t hand[14];
+        const uint8_t* m = st.misc + b * MISC;
+#pragma unroll
+        for (int j = 0; j < 14; j++) hand[j] = m[j];
+        __syncwarp();
+        gather_attacks(S, lane);
+        int ksq = -1;
+        for (int s = lane; s < 81; s += 32) if (S.bd[s] == OU) ksq = s;
+        unsigned bk = __ballot_sync(BBK_FULL, ksq >= 0);
+        ksq = __shfl_sync(BBK_FULL, ksq, bk ? __ffs(bk) - 1 : 0);
+        const bool in_check = bk && S.acnt[1][ksq] > 0;
+        build_and_emit_obs(S, lut, hand, side, in_check, obs, b, lane);
+        __syncwarp();
+    }
+}
+
+static int launch(const Params& p, cudaStream_t s) {
+    int64_t grid = (p.n + kWarps - 1) / kWarps;
+    if (grid > 148 * 12) grid = 148 * 12;
+    step_kernel<<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, 0, s>>>(p);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace shogi
+
+extern "C" {
+
+int bbk_shogi_init(const bbk_cols* out, const bbk_shogi_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
+                   const uint64_t* slot_keys, int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    shogi::Params p{};
+    p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.force_reset = 1;
+    return shogi::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_shogi_step(const bbk_cols* in, const bbk_shogi_state* in_s, const bbk_cols* out, const bbk_shogi_state* out_s,
+                   const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                   int32_t max_steps, void* stream) {
+    if (n <= 0) return 0;
+    shogi::Params p{};
+    p.in = *in; p.in_s = *in_s; p.out = *out; p.out_s = *out_s; p.actions = actions; p.slot_keys = slot_keys;
+    p.n = n; p.slot0 = slot0; p.key = key_state; p.max_steps = max_steps; p.force_reset = 0;
+    return shogi::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_shogi_observe(const bbk_shogi_state* s, const int32_t* step_count, const uint8_t* role, float* obs, int64_t n,
+                      void* stream) {
+    (void)step_count;
+    if (n <= 0) return 0;
+    int64_t grid = (n + shogi::kWarps - 1) / shogi::kWarps;
+    if (grid > 148 * 8) grid = 148 * 8;
+    shogi::observe_kernel<<<(unsigned)grid, shogi::kWarps * 32, 0, (cudaStream_t)stream>>>(*s, role, obs, n);
+    return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""Shogi on the device (reserved id ``shogi`` in the reference, games/__init__.py:31).
+
+There is no reference engine: rules, observation (dlshogi-style 119 planes)
+and action encoding (81 destinations x 27 directions incl. 7 drops) follow
+PAPER.md:1278-1354 with the conventions in DESIGN.md §3.4. CPU twin:
+oracle/orc_shogi.c (perft-pinned); parity against the reference is
+"unpinned" for shogi.
+
+Device state per slot: board[96] absolute piece codes, misc[16] (hands,
+side to move, repetition count) and a per-lineage in-place log of 64-bit
+position keys by ply (four-fold repetition).
+"""
+
+from __future__ import annotations
+
+from .. import _native as nat
+from ..core import GameDef, GameSpec
+from ._device import DeviceV, Lineage, _torch
+from .chess import RingKernel, RingStore
+
+
+class ShogiCoreView:
+    __slots__ = ("board", "hands", "role_to_move", "rep", "terminal", "rewards", "mask")
+
+    def __init__(self, board, hands, role_to_move, rep, terminal, rewards, mask):
+        self.board = board
+        self.hands = hands
+        self.role_to_move = role_to_move
+        self.rep = rep
+        self.terminal = terminal
+        self.rewards = rewards
+        self.mask = mask
+
+    def encode(self) -> bytes:
+        """board[81] + hands[2][7] + side to move + repetition count (oracle orc_shogi_encode)."""
+        return self.board + self.hands + bytes([self.role_to_move, self.rep])
+
+
+class ShogiKernel(RingKernel):
+    game_id = "shogi"
+    prefix = "shogi"
+    num_actions = 2187
+    obs_shape = (9, 9, 119)
+    board_bytes = 96
+    misc_bytes = 16
+
+    def state_struct(self, v: DeviceV, i: int | None = None):
+        h = v.store.hist
+        if i is None:
+            return nat.ShogiState(nat.ptr(v.priv.board), nat.ptr(v.priv.misc), nat.ptr(h), h.shape[1])
+        return nat.ShogiState(nat.ptr(v.priv.board[i:i + 1]), nat.ptr(v.priv.misc[i:i + 1]), nat.ptr(h[i:i + 1]),
+                              h.shape[1])
+
+    def launch_init(self, v, ks, sk):
+        torch = _torch()
+        v.store = RingStore(torch.empty((v.n, int(v.limit) + 2), dtype=torch.int64, device=v.device))
+        v.store.lineage = Lineage(v.uid)
+        nat.check(nat.lib().bbk_shogi_init(self.cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
+                                           nat.stream_handle(v.device)), "bbk_shogi_init")
+
+    def prepare_step(self, v, out):
+        if out.limit + 2 > v.store.hist.shape[1]:
+            raise ValueError("max_steps exceeds the position-log capacity of this batch")
+        super().prepare_step(v, out)
+
+    def observe_at(self, gdef, v, i, role):
+        s = self.host_snapshot(v)
+        if v.dev.observation is not None and int(role) == int(s["misc"][i][14]):
+            return v.observation[i].copy()
+        return super(RingKernel, self).observe_at(gdef, v, i, role)
+
+    def core_view(self, s, i, p2r, rewards, mask, terminal):
+        import numpy as np
+
+        m = s["misc"][i]
+        bits = 0 if (terminal or s["truncated"][i]) else int.from_bytes(
+            np.packbits(mask, bitorder="little").tobytes(), "little")
+        return ShogiCoreView(bytes(s["board"][i][:81]), bytes(m[:14]), int(m[14]), int(m[15]), terminal,
+                             self.role_rewards(p2r, rewards), bits)
+
+
+GAME = GameDef(
+    spec=GameSpec("shogi", 2, (9, 9, 119), 2187),
+    max_steps=256,
+    batch_kernel=ShogiKernel(),
+)

@@ -62,6 +62,8 @@ def run_pair(oracle, game, n, steps, seed=0, max_steps=None, obs_every=1, enc_ev
     ("backgammon", 16, 200, 25),
     ("chess", 16, 300, None),
     ("chess", 8, 120, 40),
+    ("shogi", 16, 300, None),
+    ("shogi", 8, 120, 40),
 ])
 def test_device_matches_oracle(oracle, game, n, steps, max_steps):
     run_pair(oracle, game, n, steps, seed=3, max_steps=max_steps)
@@ -99,15 +101,15 @@ def test_baseline_config1_go9_b1024_to_all_finished():
     assert done.all()
 
 
-@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess"])
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"])
 def test_large_batch_vs_oracle_columns(oracle, game):
     """Thousands of slots, columns + observations checked against the oracle every step."""
-    n = 2048 if game not in ("go_19x19", "chess") else 1024
+    n = 2048 if game not in ("go_19x19", "chess", "shogi") else 1024
     steps = 60 if game != "backgammon" else 150
     run_pair(oracle, game, n, steps, seed=11, obs_every=10, enc_every=30)
 
 
-@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess"])
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"])
 def test_batch_step_equals_scalar_steps(game):
     """Port of reference test_core.py:179-196 on the device scalar API."""
     root = bb.RngKey(71)
