@@ -247,7 +247,7 @@ static int action_of(smove m) {
     if (m.drop) return (20 + m.drop - 1) * 81 + m.to;
     int fr_ = m.from / 9, fc = m.from % 9, tr = m.to / 9, tc = m.to % 9;
     int dr = tr - fr_, dc = tc - fc, dir;
-    if (dr == -2) dir = dc < 0 ? 8 : 9;
+    if (dr == -2 && (dc == 1 || dc == -1)) dir = dc < 0 ? 8 : 9;   /* knight jump */
     else {
         int sr = (dr > 0) - (dr < 0), sc = (dc > 0) - (dc < 0);
         static const int DIRMAP[3][3] = {{1, 0, 2}, {3, -1, 4}, {6, 5, 7}};

@@ -70,3 +70,12 @@ def test_random_play_invariants(oracle):
         obs = c["observation"]
         assert (obs[..., 7].sum(axis=(1, 2)) == 1).all() and (obs[..., 31 + 7].sum(axis=(1, 2)) == 1).all()
         assert s.step(s.sample_random_actions(c)) == -1
+
+
+def test_lance_slide_is_not_a_knight_code(oracle):
+    # after 1. P-9f (pawn (6,0)->(5,0)) the lance on (8,0) may slide up two squares: direction UP (0)
+    b = oracle.ShogiBatch(1).init(3)
+    b.set_sfen(0, "lnsgkgsnl/1r5b1/ppppppppp/9/9/P8/1PPPPPPPP/1B5R1/LNSGKGSNL b - 1")
+    m = b.columns()["legal_action_mask"][0]
+    assert m[0 * 81 + 6 * 9 + 0] and m[0 * 81 + 7 * 9 + 0]
+    assert not m[9 * 81 + 6 * 9 + 0]          # (the knight reaches (6,0) with code 8, legitimately)
