@@ -224,7 +224,7 @@ def run_gpu(args, rank, world, local):
         "episodes_completed": int(episodes.item()),
     }
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, gdef, kern, cur, root, t, dev, world)
+        out["e2e"] = run_e2e(args, gdef, kern, root, dev, world, slot0, B)
     if args.sweep:
         out["sweep"] = run_sweep(args, gdef, kern, dev, slot0)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -236,30 +236,29 @@ def run_gpu(args, rank, world, local):
     return out
 
 
-def run_e2e(args, gdef, kern, cur, root, t, dev, world):
-    """Same metric through the public API with host buffers.
+def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
+    """Same metric through the public API with host buffers, over the same step window.
 
-    Per step: device random policy -> D2H of the actions into pinned host
-    memory (a host agent's output) -> core.batch_step(host actions) (H2D
-    inside) -> D2H of rewards/terminated/truncated/current_player, then the
-    host reads them (synchronous, as a host RL loop does).
+    A fresh batch (same seed, same slots) is stepped W untimed + K timed steps through
+    core.batch_step. Per step: device random policy -> D2H of the actions into pinned host
+    memory (a host agent's output) -> core.batch_step(host actions) (H2D inside) -> D2H of
+    rewards/terminated/truncated/current_player, read on the host (synchronous, as a host RL
+    loop does).
     """
     import torch
 
     from paper_2303_17503_b200.core import Batch, batch_step
 
-    B = cur.n
-    batch = Batch(gdef, B, gdef.max_steps, vstate=cur)
+    batch = Batch(gdef, B, gdef.max_steps, vstate=kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0,
+                                                            device=dev))
     host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
     host_r = torch.empty((B, 2), dtype=torch.float32, pin_memory=True)
     host_f = torch.empty((B, 2), dtype=torch.uint8, pin_memory=True)
     host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
-    steps = max(4, min(args.steps, 64))
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for k in range(steps):
+    t = 0
+
+    def one():
+        nonlocal batch, t
         a = kern.random_actions(batch._v, root.child(2 * t + 1))
         host_act.copy_(a)
         batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False)
@@ -270,6 +269,15 @@ def run_e2e(args, gdef, kern, cur, root, t, dev, world):
         host_cp.copy_(d.current_player, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         t += 1
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
     dt = time.perf_counter() - t0
     if world > 1:
         import torch.distributed as dist
@@ -277,9 +285,10 @@ def run_e2e(args, gdef, kern, cur, root, t, dev, world):
         tt = torch.tensor([dt], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-    return {"value": B * world * steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
-            "d2h_bytes_per_step": (8 + 8 + 2 + 4) * B, "steps": steps,
-            "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player"}
+    return {"value": B * world * args.steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
+            "d2h_bytes_per_step": (8 + 8 + 2 + 4) * B, "steps": args.steps,
+            "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player, "
+                    "same window as value (fresh init, W warm-up, K timed)"}
 
 
 def run_sweep(args, gdef, kern, dev, slot0):

@@ -43,14 +43,23 @@ template <int N>
 struct WarpSmem {
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
+    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
     uint32_t bloom[BBK_GO_BLOOM_WORDS];
     uint64_t capx[C];
-    uint32_t par[C];
-    uint32_t gst[C];
-    uint32_t P[C + 4];
+    union {
+        struct {
+            uint32_t run[MAXR];    // (colour << 24) | (row << 16) | (start << 8) | len
+            uint32_t par[MAXR];    // union-find over run indices
+            uint32_t gst[MAXR];    // OR(lib) | OR(~lib) << 10 | HAS, at group roots
+            uint16_t root[MAXR];
+            uint8_t atari[MAXR];
+        } uf;
+        uint32_t P[C + 4];         // observation pattern (after the mask is done)
+    } u;
     alignas(16) uint16_t pat[pat_stride(N)];
     alignas(16) uint8_t mb[((A + 47) & ~15)];
-    uint32_t capbits[32];
+    uint32_t rX[32], rY[32], rSX[32], rSY[32], rE[32], rcap[32];
+    int32_t roff[33];
     uint32_t rowB[32];
     uint32_t rowW[32];
     uint64_t hit[32];
@@ -161,81 +170,121 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 // Legal mask rows for the side to move (go.py:121-174, allow_self_capture
 // off). X = mover's stones, Y = opponent's stones, E = empties (row bits of
 // this lane). `zX`/`zY` are the zobrist tables of the two colours.
+//
+// Group analysis (go.py:45-80 restated for what the mask needs): every
+// horizontal run of stones is a union-find node. Runs are laid out as a flat
+// list (row-major, X runs then Y runs per row) so that the union / flatten /
+// liberty / classification passes stride lanes over RUNS, not rows -- the work
+// is balanced no matter how the stones are distributed over the rows.
 template <int N>
 __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_t* zY, uint32_t X, uint32_t Y,
                                uint32_t E, uint64_t h, const uint64_t* hist, int nscan, uint64_t extra, int lane) {
     constexpr uint32_t ROW = (1u << N) - 1u;
+    auto& U = S.u.uf;
     const int r = lane;
     const uint32_t SX = X & ~(X << 1), SY = Y & ~(Y << 1);
-    // 1. run starts are union-find nodes
-    for (uint32_t s_ = SX | SY; s_; s_ &= s_ - 1) {
-        uint32_t node = r * N + (__ffs(s_) - 1);
-        S.par[node] = node;
-        S.gst[node] = 0u;
-    }
-    S.capbits[lane] = 0u;
-    __syncwarp();
-    // 2. hook each run to the vertically overlapping runs of the row above
-    {
-        const uint32_t Xu = up_row(X, lane), Yu = up_row(Y, lane);
-        const uint32_t SXu = Xu & ~(Xu << 1), SYu = Yu & ~(Yu << 1);
+    const int nx = __popc(SX), cnt = nx + __popc(SY);
+    int off = cnt;   // exclusive prefix sum of run counts over rows
 #pragma unroll
-        for (int col = 0; col < 2; col++) {
-            const uint32_t Z = col ? Y : X, Zu = col ? Yu : Xu, SZ = col ? SY : SX, SZu = col ? SYu : SXu;
-            for (uint32_t s_ = SZ; s_; s_ &= s_ - 1) {
-                int s = __ffs(s_) - 1;
-                uint32_t V = run_at(Z, s) & Zu;
-                while (V) {
-                    int c = __ffs(V) - 1;
-                    int st = 31 - __clz(SZu & ((2u << c) - 1u));
-                    V &= ~run_at(Zu, st);
-                    uf_union(S.par, r * N + s, (r - 1) * N + st);
-                }
-            }
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(BBK_FULL, off, o);
+        if (lane >= o) off += t;
+    }
+    const int total = __shfl_sync(BBK_FULL, off, 31);
+    off -= cnt;
+    S.rX[lane] = X; S.rY[lane] = Y; S.rSX[lane] = SX; S.rSY[lane] = SY; S.rE[lane] = E; S.rcap[lane] = 0u;
+    S.roff[lane] = off;
+    if (lane == 31) S.roff[32] = total;
+    {   // this row's runs -> list
+        int k = off;
+        for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++) {
+            int s = __ffs(s_) - 1;
+            U.run[k] = (0u << 24) | ((uint32_t)r << 16) | ((uint32_t)s << 8) | (uint32_t)(__ffs(~(X >> s)) - 1);
         }
+        for (uint32_t s_ = SY; s_; s_ &= s_ - 1, k++) {
+            int s = __ffs(s_) - 1;
+            U.run[k] = (1u << 24) | ((uint32_t)r << 16) | ((uint32_t)s << 8) | (uint32_t)(__ffs(~(Y >> s)) - 1);
+        }
+    }
+    for (int i = lane; i < total; i += 32) { U.par[i] = (uint32_t)i; U.gst[i] = 0u; }
+    __syncwarp();
+    // 1. hook each run to the overlapping same-colour runs of the row above
+    for (int i = lane; i < total; i += 32) {
+        const uint32_t e = U.run[i];
+        const int rr = (e >> 16) & 0xFF;
+        if (rr == 0) continue;
+        const int col = e >> 24, s = (e >> 8) & 0xFF, len = e & 0xFF;
+        const uint32_t Zu = col ? S.rY[rr - 1] : S.rX[rr - 1];
+        const uint32_t Su = col ? S.rSY[rr - 1] : S.rSX[rr - 1];
+        const int base = S.roff[rr - 1] + (col ? __popc(S.rSX[rr - 1]) : 0);
+        uint32_t V = (((1u << len) - 1u) << s) & Zu;
+        while (V) {
+            const int c = __ffs(V) - 1;
+            const int st = 31 - __clz(Su & ((2u << c) - 1u));
+            V &= ~run_at(Zu, st);
+            uf_union(U.par, (uint32_t)i, (uint32_t)(base + __popc(Su & ((1u << st) - 1u))));
+        }
+    }
+    __syncwarp();
+    // 2. flatten: root of every run (chains are static now; compress while walking)
+    for (int i = lane; i < total; i += 32) {
+        uint32_t x = (uint32_t)i;
+        while (true) {   // path halving: every write points at an ancestor, so racing lanes stay consistent
+            const uint32_t p = U.par[x];
+            if (p == x) break;
+            const uint32_t gp = U.par[p];
+            U.par[x] = gp;
+            x = gp;
+        }
+        U.root[i] = (uint16_t)x;
     }
     __syncwarp();
     // 3. liberty position OR-stats per group root
-    const uint32_t Eu = up_row(E, lane), Ed = dn_row(E, lane);
-    for (uint32_t s_ = SX | SY; s_; s_ &= s_ - 1) {
-        int s = __ffs(s_) - 1;
-        uint32_t run = run_at((SX >> s) & 1 ? X : Y, s);
-        uint32_t up = run & Eu, dn = run & Ed, sd = ((run << 1) | (run >> 1)) & E;
+    for (int i = lane; i < total; i += 32) {
+        const uint32_t e = U.run[i];
+        const int rr = (e >> 16) & 0xFF, s = (e >> 8) & 0xFF, len = e & 0xFF;
+        const uint32_t run = ((1u << len) - 1u) << s;
+        const uint32_t up = rr > 0 ? run & S.rE[rr - 1] : 0u, dn = run & S.rE[rr + 1];
+        const uint32_t sd = ((run << 1) | (run >> 1)) & S.rE[rr];
         if (!(up | dn | sd)) continue;
-        uint32_t lo = up ? (r - 1) * N + __ffs(up) - 1 : sd ? r * N + __ffs(sd) - 1 : (r + 1) * N + __ffs(dn) - 1;
-        uint32_t hi = dn ? (r + 1) * N + 31 - __clz(dn) : sd ? r * N + 31 - __clz(sd) : (r - 1) * N + 31 - __clz(up);
-        uint32_t root = uf_find(S.par, r * N + s);
-        atomicOr(&S.gst[root], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
+        const uint32_t lo = up ? (rr - 1) * N + __ffs(up) - 1 : sd ? rr * N + __ffs(sd) - 1 : (rr + 1) * N + __ffs(dn) - 1;
+        const uint32_t hi = dn ? (rr + 1) * N + 31 - __clz(dn) : sd ? rr * N + 31 - __clz(sd) : (rr - 1) * N + 31 - __clz(up);
+        atomicOr(&U.gst[U.root[i]], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
     __syncwarp();
-    // 4. atari classification. NA: mover stones whose group has >= 2 libs.
-    uint32_t NA = 0u, atY = 0u;
-    for (uint32_t s_ = SX; s_; s_ &= s_ - 1) {
-        int s = __ffs(s_) - 1;
-        uint32_t g = S.gst[uf_find(S.par, r * N + s)];
-        if ((g & (g >> 10) & 0x3FFu) != 0u) NA |= run_at(X, s);
-    }
-    for (uint32_t s_ = SY; s_; s_ &= s_ - 1) {
-        int s = __ffs(s_) - 1;
-        uint32_t g = S.gst[uf_find(S.par, r * N + s)];
-        if ((g & 0x80000000u) && (g & (g >> 10) & 0x3FFu) == 0u) {
-            uint32_t lib = g & 0x3FFu;
-            atY |= 1u << s;
+    // 4. atari classification; capture liberties of opponent atari groups
+    for (int i = lane; i < total; i += 32) {
+        const uint32_t g = U.gst[U.root[i]];
+        const bool at = !(g & 0x80000000u) || (g & (g >> 10) & 0x3FFu) == 0u;
+        U.atari[i] = at;
+        if ((U.run[i] >> 24) && at && (g & 0x80000000u)) {
+            const uint32_t lib = g & 0x3FFu;
             S.capx[lib] = 0ull;
-            atomicOr(&S.capbits[lib / N], 1u << (lib % N));
+            atomicOr(&S.rcap[lib / N], 1u << (lib % N));
         }
     }
     __syncwarp();
-    for (uint32_t s_ = atY; s_; s_ &= s_ - 1) {
-        int s = __ffs(s_) - 1;
-        uint32_t lib = S.gst[uf_find(S.par, r * N + s)] & 0x3FFu;
+    for (int i = lane; i < total; i += 32) {
+        const uint32_t e = U.run[i];
+        if (!(e >> 24) || !U.atari[i]) continue;
+        const uint32_t g = U.gst[U.root[i]];
+        if (!(g & 0x80000000u)) continue;
+        const int rr = (e >> 16) & 0xFF, s = (e >> 8) & 0xFF, len = e & 0xFF;
         uint64_t x = 0ull;
-        for (uint32_t b = run_at(Y, s); b; b &= b - 1) x ^= zY[r * N + __ffs(b) - 1];
-        atomicXor(reinterpret_cast<unsigned long long*>(&S.capx[lib]), (unsigned long long)x);
+        for (int q = 0; q < len; q++) x ^= zY[rr * N + s + q];
+        atomicXor(reinterpret_cast<unsigned long long*>(&S.capx[g & 0x3FFu]), (unsigned long long)x);
     }
     __syncwarp();
-    // 5. candidates + superko filter
-    const uint32_t capb = lane < N ? S.capbits[lane] : 0u;
+    // NA: mover stones whose group has >= 2 liberties (this row's X runs)
+    uint32_t NA = 0u;
+    {
+        int k = off;
+        for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++)
+            if (!U.atari[k]) NA |= run_at(X, __ffs(s_) - 1);
+    }
+    // 5. candidates + superko filter (row-parallel)
+    const uint32_t Eu = up_row(E, lane), Ed = dn_row(E, lane);
+    const uint32_t capb = lane < N ? S.rcap[lane] : 0u;
     const uint32_t NAu = up_row(NA, lane), NAd = dn_row(NA, lane);
     const uint32_t nb = ((E << 1) | (E >> 1) | Eu | Ed | (NA << 1) | (NA >> 1) | NAu | NAd) & ROW;
     const uint32_t cand = E & (capb | nb);
@@ -286,9 +335,9 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
     for (int i = lane; i < C; i += 32) {
         uint32_t v = S.pat[i];
         if (role) v = ((v & 0x5555u) << 1) | ((v >> 1) & 0x5555u);
-        S.P[i] = v | ((uint32_t)role << 16);
+        S.u.P[i] = v | ((uint32_t)role << 16);
     }
-    if (lane < 4) S.P[C + lane] = 0u;
+    if (lane < 4) S.u.P[C + lane] = 0u;
     __syncwarp();
     const int64_t F0 = b * (int64_t)NF;
     const int64_t a0 = (F0 + 3) & ~(int64_t)3, a1 = (F0 + NF) & ~(int64_t)3;
@@ -298,14 +347,14 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
         if (ok) {
             uint32_t fi = (uint32_t)(f - F0);
             uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;
-            obs[f] = (float)((S.P[c] >> k) & 1u);
+            obs[f] = (float)((S.u.P[c] >> k) & 1u);
         }
     }
     float4* o4 = reinterpret_cast<float4*>(obs);
     for (int64_t j = (a0 >> 2) + lane; j < (a1 >> 2); j += 32) {
         uint32_t fi = (uint32_t)((j << 2) - F0);
         uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;   // fi/17, exact for fi < 65536
-        uint64_t w = (uint64_t)S.P[c] | ((uint64_t)S.P[c + 1] << 17);
+        uint64_t w = (uint64_t)S.u.P[c] | ((uint64_t)S.u.P[c + 1] << 17);
         o4[j] = lut[(uint32_t)(w >> k) & 15u];
     }
     __syncwarp();
