@@ -96,24 +96,27 @@ __device__ bool attacked_mod(const uint8_t* bd, int sq, int by, int e1, int e2, 
     return false;
 }
 
+// (dr+2)*5 + (df+2) -> knight plane 56+k (KN_DR/KN_DF order), or -1;
+// (sr+1)*3 + (sf+1) -> queen direction index (DIR_DR/DIR_DF order)
+__device__ __constant__ int8_t KN_PLANE[25] = {-1, 60, -1, 59, -1, 61, -1, -1, -1, 58, -1, -1, -1, -1, -1,
+                                               62, -1, -1, -1, 57, -1, 63, -1, 56, -1};
+__device__ __constant__ int8_t QDIR[9] = {5, 4, 3, 6, -1, 2, 7, 0, 1};
+
 // AlphaZero action index in the mover's frame.
 __device__ __forceinline__ int action_of(int fl, int from, int to, int promo) {
-    int f = from ^ fl, t = to ^ fl;
-    int dr = (t >> 3) - (f >> 3), df = (t & 7) - (f & 7);
+    const int f = from ^ fl, t = to ^ fl;
+    const int dr = (t >> 3) - (f >> 3), df = (t & 7) - (f & 7);
     int plane;
     if (promo && promo != Q) {
         plane = 64 + 3 * (promo == N ? 0 : promo == B ? 1 : 2) + (df + 1);
     } else {
-        int adr = dr < 0 ? -dr : dr, adf = df < 0 ? -df : df;
-        if ((adr == 2 && adf == 1) || (adr == 1 && adf == 2)) {
-            int k = 0;
-            for (int j = 0; j < 8; j++) if (KN_DR[j] == dr && KN_DF[j] == df) k = j;
-            plane = 56 + k;
+        const int adr = dr < 0 ? -dr : dr, adf = df < 0 ? -df : df;
+        const int kn = (adr <= 2 && adf <= 2) ? KN_PLANE[(dr + 2) * 5 + (df + 2)] : -1;
+        if (kn >= 0) {
+            plane = kn;
         } else {
-            int dist = adr > adf ? adr : adf;
-            int sr = (dr > 0) - (dr < 0), sf = (df > 0) - (df < 0);
-            int d = 0;
-            for (int j = 0; j < 8; j++) if (DIR_DR[j] == sr && DIR_DF[j] == sf) d = j;
+            const int dist = adr > adf ? adr : adf;
+            const int d = QDIR[((dr > 0) - (dr < 0) + 1) * 3 + ((df > 0) - (df < 0) + 1)];
             plane = d * 7 + dist - 1;
         }
     }
@@ -498,25 +501,18 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
             }
             __syncwarp();
         }
-        const float cnt113 = (float)step / 512.0f, cnt118 = (float)halfmove / 100.0f;
         if (p.out.observation) {
-            float4* o4 = reinterpret_cast<float4*>(p.out.observation + b * (int64_t)NF);
-            for (int j = lane; j < NF / 4; j += 32) {
-                const uint32_t nib = (S.bits[j >> 3] >> ((j & 7) * 4)) & 15u;
-                float4 val = lut[nib];
-                const uint32_t f0 = 4u * (uint32_t)j;
-                const uint32_t cc = (f0 * 8812u) >> 20;      // f0 / 119 (exact for f0 < 7616+)
-                const int k0 = (int)(f0 - 119u * cc);
-                float* vp = reinterpret_cast<float*>(&val);
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    int kq = k0 + q;
-                    if (kq >= 119) kq -= 119;
-                    if (kq == 113) vp[q] = cnt113;
-                    else if (kq == 118) vp[q] = cnt118;
-                }
-                o4[j] = val;
-            }
+            // binary planes through the LUT, then the two count planes (113, 118) of the
+            // 64 squares as scalar stores, ordered after the vector stores by __syncwarp
+            float* orec = p.out.observation + b * (int64_t)NF;
+            float4* o4 = reinterpret_cast<float4*>(orec);
+            for (int j = lane; j < NF / 4; j += 32) o4[j] = lut[(S.bits[j >> 3] >> ((j & 7) * 4)) & 15u];
+            __syncwarp();
+            const float cnt113 = (float)step / 512.0f, cnt118 = (float)halfmove / 100.0f;
+            orec[119 * lane + 113] = cnt113;
+            orec[119 * (lane + 32) + 113] = cnt113;
+            orec[119 * lane + 118] = cnt118;
+            orec[119 * (lane + 32) + 118] = cnt118;
         }
         // ---- mask: zero when finished, else the staged bytes
         if (terminal || truncated) {

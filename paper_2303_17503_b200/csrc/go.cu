@@ -65,10 +65,41 @@ struct WarpSmem {
     uint64_t hit[32];
 };
 
+// Zobrist tables (go.py:20-25): zob[2*cell + colour] = mix64(base + 2*cell + colour),
+// base = 0x60D00D60C0FFEE00 + N. Evaluated at compile time into read-only global
+// memory (L1-cached via __ldg) so they cost no shared memory.
+struct ZobTables {
+    uint64_t v[3][2 * 19 * 19];
+};
+__host__ __device__ constexpr uint64_t cmix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ULL;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+constexpr ZobTables make_zob() {
+    ZobTables z{};
+    const int sizes[3] = {9, 13, 19};
+    for (int k = 0; k < 3; k++) {
+        const int n = sizes[k];
+        const uint64_t base = 0x60D00D60C0FFEE00ULL + (uint64_t)n;
+        for (int i = 0; i < 2 * n * n; i++) {
+            const int cell = i % (n * n), colour = i / (n * n);   // [0,C) black, [C,2C) white
+            z.v[k][i] = cmix64(base + 2ull * (uint64_t)cell + (uint64_t)colour);
+        }
+    }
+    return z;
+}
+__device__ const ZobTables g_zob = make_zob();
+template <int N>
+__device__ __forceinline__ const uint64_t* zob_table() {
+    return g_zob.v[N == 9 ? 0 : N == 13 ? 1 : 2];
+}
+
 template <int N>
 struct BlockSmem {
     static constexpr int C = N * N;
-    uint64_t zob[2 * C];     // [0,C) black, [C,2C) white  (go.py:20-25)
     float4 lut[16];
     WarpSmem<N> w[kWarps];
 };
@@ -98,11 +129,23 @@ __device__ __forceinline__ uint32_t uf_find(volatile uint32_t* par, uint32_t x) 
     return x;
 }
 
+// find with path halving; racing lanes only ever re-point a node at one of its
+// ancestors, so the forest stays valid while other lanes hook roots with CAS.
+__device__ __forceinline__ uint32_t uf_find_halve(volatile uint32_t* par, uint32_t x) {
+    while (true) {
+        const uint32_t p = par[x];
+        if (p == x) return x;
+        const uint32_t gp = par[p];
+        if (gp != p) par[x] = gp;
+        x = gp;
+    }
+}
+
 __device__ __forceinline__ void uf_union(uint32_t* par, uint32_t a, uint32_t b) {
     volatile uint32_t* vp = par;
     while (true) {
-        a = uf_find(vp, a);
-        b = uf_find(vp, b);
+        a = uf_find_halve(vp, a);
+        b = uf_find_halve(vp, b);
         if (a == b) return;
         if (a < b) { uint32_t t = a; a = b; b = t; }
         uint32_t old = atomicCAS(&par[a], a, b);
@@ -271,8 +314,11 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
         if (!(g & 0x80000000u)) continue;
         const int rr = (e >> 16) & 0xFF, s = (e >> 8) & 0xFF, len = e & 0xFF;
         uint64_t x = 0ull;
-        for (int q = 0; q < len; q++) x ^= zY[rr * N + s + q];
-        atomicXor(reinterpret_cast<unsigned long long*>(&S.capx[g & 0x3FFu]), (unsigned long long)x);
+        for (int q = 0; q < len; q++) x ^= __ldg(zY + rr * N + s + q);
+        // XOR is bitwise: two native 32-bit shared atomics instead of a 64-bit one
+        uint32_t* cx = reinterpret_cast<uint32_t*>(&S.capx[g & 0x3FFu]);
+        atomicXor(cx, (uint32_t)x);
+        atomicXor(cx + 1, (uint32_t)(x >> 32));
     }
     __syncwarp();
     // NA: mover stones whose group has >= 2 liberties (this row's X runs)
@@ -292,7 +338,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
     for (uint32_t c_ = cand; c_; c_ &= c_ - 1) {
         int p = __ffs(c_) - 1;
         int cell = r * N + p;
-        uint64_t h2 = h ^ zX[cell];
+        uint64_t h2 = h ^ __ldg(zX + cell);
         if ((capb >> p) & 1u) h2 ^= S.capx[cell];
         if (bloom_maybe(S.bloom, h2)) pend |= 1u << p;
         else legal |= 1u << p;
@@ -303,7 +349,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
         uint64_t h2 = 0ull;
         if (pend) {
             int cell = r * N + p;
-            h2 = h ^ zX[cell];
+            h2 = h ^ __ldg(zX + cell);
             if ((capb >> p) & 1u) h2 ^= S.capx[cell];
             S.hit[lane] = h2;
         }
@@ -362,12 +408,6 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
 
 template <int N>
 __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
-    constexpr int C = N * N;
-    const uint64_t base = 0x60D00D60C0FFEE00ULL + (uint64_t)N;   // go.py:22
-    for (int i = threadIdx.x; i < 2 * C; i += blockDim.x) {
-        int cell = i < C ? i : i - C, colour = i < C ? 0 : 1;
-        B.zob[i] = mix64(base + 2ull * (uint64_t)cell + (uint64_t)colour);
-    }
     if (threadIdx.x < 16) {
         uint32_t n = threadIdx.x;
         B.lut[n] = make_float4((float)(n & 1), (float)((n >> 1) & 1), (float)((n >> 2) & 1), (float)((n >> 3) & 1));
@@ -446,8 +486,8 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                 uint32_t M = role == 0 ? Bk : Wh, O = role == 0 ? Wh : Bk;
                 if (lane == ra) M |= 1u << ca;
                 const uint32_t E0 = ~(M | O) & rowm;
-                const uint64_t* zM = B.zob + role * C;
-                const uint64_t* zO = B.zob + (1 - role) * C;
+                const uint64_t* zM = zob_table<N>() + role * C;
+                const uint64_t* zO = zob_table<N>() + (1 - role) * C;
                 uint64_t capxor = 0ull;
                 uint32_t visited = 0u, dead = 0u;
                 const int qr_[4] = {ra - 1, ra + 1, ra, ra};
@@ -474,9 +514,9 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                     visited |= F;
                     if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E0) != 0u)) dead |= F;
                 }
-                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zO[lane * N + __ffs(d_) - 1];
+                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= __ldg(zO + lane * N + __ffs(d_) - 1);
                 O &= ~dead;
-                const uint64_t h2 = h ^ zM[a] ^ warp_xor64(capxor);
+                const uint64_t h2 = h ^ __ldg(zM + a) ^ warp_xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
                 if (lane == 0) {
                     hist[hlen] = h2;
@@ -507,7 +547,8 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            legal = legal_rows<N>(S, B.zob + role * C, B.zob + (1 - role) * C, X, Y, E, h, hist, nscan, extra, lane);
+            legal = legal_rows<N>(S, zob_table<N>() + role * C, zob_table<N>() + (1 - role) * C, X, Y, E, h, hist, nscan,
+                                  extra, lane);
         }
         // stage mask bytes at the destination's 16-byte phase and emit
         const int64_t mstart = b * (int64_t)A;
