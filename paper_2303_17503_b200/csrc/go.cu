@@ -46,23 +46,23 @@ struct WarpSmem {
     static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
     uint32_t bloom[BBK_GO_BLOOM_WORDS];
     uint64_t capx[C];
+    // Phase-multiplexed scratch (each member is dead before the next one is written):
+    // group analysis -> superko hits -> staged mask bytes -> observation pattern.
     union {
         struct {
-            uint32_t run[MAXR];    // (colour << 24) | (row << 16) | (start << 8) | len
-            uint32_t par[MAXR];    // union-find over run indices
+            uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
+            uint16_t par[MAXR];    // union-find over run indices
             uint32_t gst[MAXR];    // OR(lib) | OR(~lib) << 10 | HAS, at group roots
             uint16_t root[MAXR];
             uint8_t atari[MAXR];
         } uf;
-        uint32_t P[C + 4];         // observation pattern (after the mask is done)
+        uint64_t hit[32];
+        alignas(16) uint8_t mb[((A + 47) & ~15)];
+        uint32_t P[C + 4];
     } u;
     alignas(16) uint16_t pat[pat_stride(N)];
-    alignas(16) uint8_t mb[((A + 47) & ~15)];
-    uint32_t rX[32], rY[32], rSX[32], rSY[32], rE[32], rcap[32];
+    uint32_t rX[32], rY[32], rSX[32], rSY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
     int32_t roff[33];
-    uint32_t rowB[32];
-    uint32_t rowW[32];
-    uint64_t hit[32];
 };
 
 // Zobrist tables (go.py:20-25): zob[2*cell + colour] = mix64(base + 2*cell + colour),
@@ -131,24 +131,25 @@ __device__ __forceinline__ uint32_t uf_find(volatile uint32_t* par, uint32_t x) 
 
 // find with path halving; racing lanes only ever re-point a node at one of its
 // ancestors, so the forest stays valid while other lanes hook roots with CAS.
-__device__ __forceinline__ uint32_t uf_find_halve(volatile uint32_t* par, uint32_t x) {
+__device__ __forceinline__ uint32_t uf_find_halve(volatile uint16_t* par, uint32_t x) {
     while (true) {
         const uint32_t p = par[x];
         if (p == x) return x;
         const uint32_t gp = par[p];
-        if (gp != p) par[x] = gp;
+        if (gp != p) par[x] = (uint16_t)gp;
         x = gp;
     }
 }
 
-__device__ __forceinline__ void uf_union(uint32_t* par, uint32_t a, uint32_t b) {
-    volatile uint32_t* vp = par;
+__device__ __forceinline__ void uf_union(uint16_t* par, uint32_t a, uint32_t b) {
+    volatile uint16_t* vp = par;
     while (true) {
         a = uf_find_halve(vp, a);
         b = uf_find_halve(vp, b);
         if (a == b) return;
         if (a < b) { uint32_t t = a; a = b; b = t; }
-        uint32_t old = atomicCAS(&par[a], a, b);
+        const uint32_t old = atomicCAS(reinterpret_cast<unsigned short*>(&par[a]), (unsigned short)a,
+                                       (unsigned short)b);
         if (old == a) return;
     }
 }
@@ -242,21 +243,23 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
-            U.run[k] = (0u << 24) | ((uint32_t)r << 16) | ((uint32_t)s << 8) | (uint32_t)(__ffs(~(X >> s)) - 1);
+            U.run[k] = (uint16_t)((0u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(X >> s)) - 1));
         }
         for (uint32_t s_ = SY; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
-            U.run[k] = (1u << 24) | ((uint32_t)r << 16) | ((uint32_t)s << 8) | (uint32_t)(__ffs(~(Y >> s)) - 1);
+            U.run[k] = (uint16_t)((1u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(Y >> s)) - 1));
         }
     }
-    for (int i = lane; i < total; i += 32) { U.par[i] = (uint32_t)i; U.gst[i] = 0u; }
+    for (int i = lane; i < total; i += 32) { U.par[i] = (uint16_t)i; U.gst[i] = 0u; }
+    for (int i = lane; i < (N * N + 1) / 2; i += 32)
+        reinterpret_cast<uint4*>(S.capx)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     // 1. hook each run to the overlapping same-colour runs of the row above
     for (int i = lane; i < total; i += 32) {
         const uint32_t e = U.run[i];
-        const int rr = (e >> 16) & 0xFF;
+        const int rr = (e >> 10) & 31;
         if (rr == 0) continue;
-        const int col = e >> 24, s = (e >> 8) & 0xFF, len = e & 0xFF;
+        const int col = e >> 15, s = (e >> 5) & 31, len = e & 31;
         const uint32_t Zu = col ? S.rY[rr - 1] : S.rX[rr - 1];
         const uint32_t Su = col ? S.rSY[rr - 1] : S.rSX[rr - 1];
         const int base = S.roff[rr - 1] + (col ? __popc(S.rSX[rr - 1]) : 0);
@@ -269,56 +272,45 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
         }
     }
     __syncwarp();
-    // 2. flatten: root of every run (chains are static now; compress while walking)
+    // 2. flatten (path halving; chains are static now) + liberty OR-stats per group root
     for (int i = lane; i < total; i += 32) {
         uint32_t x = (uint32_t)i;
-        while (true) {   // path halving: every write points at an ancestor, so racing lanes stay consistent
+        while (true) {   // every write points at an ancestor, so racing lanes stay consistent
             const uint32_t p = U.par[x];
             if (p == x) break;
             const uint32_t gp = U.par[p];
-            U.par[x] = gp;
+            U.par[x] = (uint16_t)gp;
             x = gp;
         }
         U.root[i] = (uint16_t)x;
-    }
-    __syncwarp();
-    // 3. liberty position OR-stats per group root
-    for (int i = lane; i < total; i += 32) {
         const uint32_t e = U.run[i];
-        const int rr = (e >> 16) & 0xFF, s = (e >> 8) & 0xFF, len = e & 0xFF;
+        const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
         const uint32_t run = ((1u << len) - 1u) << s;
         const uint32_t up = rr > 0 ? run & S.rE[rr - 1] : 0u, dn = run & S.rE[rr + 1];
         const uint32_t sd = ((run << 1) | (run >> 1)) & S.rE[rr];
         if (!(up | dn | sd)) continue;
         const uint32_t lo = up ? (rr - 1) * N + __ffs(up) - 1 : sd ? rr * N + __ffs(sd) - 1 : (rr + 1) * N + __ffs(dn) - 1;
         const uint32_t hi = dn ? (rr + 1) * N + 31 - __clz(dn) : sd ? rr * N + 31 - __clz(sd) : (rr - 1) * N + 31 - __clz(up);
-        atomicOr(&U.gst[U.root[i]], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
+        atomicOr(&U.gst[x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
     __syncwarp();
-    // 4. atari classification; capture liberties of opponent atari groups
+    // 3. atari classification; capture liberties (+ zobrist XOR) of opponent atari groups
     for (int i = lane; i < total; i += 32) {
         const uint32_t g = U.gst[U.root[i]];
         const bool at = !(g & 0x80000000u) || (g & (g >> 10) & 0x3FFu) == 0u;
         U.atari[i] = at;
-        if ((U.run[i] >> 24) && at && (g & 0x80000000u)) {
-            const uint32_t lib = g & 0x3FFu;
-            S.capx[lib] = 0ull;
-            atomicOr(&S.rcap[lib / N], 1u << (lib % N));
-        }
-    }
-    __syncwarp();
-    for (int i = lane; i < total; i += 32) {
         const uint32_t e = U.run[i];
-        if (!(e >> 24) || !U.atari[i]) continue;
-        const uint32_t g = U.gst[U.root[i]];
-        if (!(g & 0x80000000u)) continue;
-        const int rr = (e >> 16) & 0xFF, s = (e >> 8) & 0xFF, len = e & 0xFF;
-        uint64_t x = 0ull;
-        for (int q = 0; q < len; q++) x ^= __ldg(zY + rr * N + s + q);
-        // XOR is bitwise: two native 32-bit shared atomics instead of a 64-bit one
-        uint32_t* cx = reinterpret_cast<uint32_t*>(&S.capx[g & 0x3FFu]);
-        atomicXor(cx, (uint32_t)x);
-        atomicXor(cx + 1, (uint32_t)(x >> 32));
+        if ((e >> 15) && at && (g & 0x80000000u)) {
+            const uint32_t lib = g & 0x3FFu;
+            atomicOr(&S.rcap[lib / N], 1u << (lib % N));
+            const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
+            uint64_t x = 0ull;
+            for (int q = 0; q < len; q++) x ^= __ldg(zY + rr * N + s + q);
+            // XOR is bitwise: two native 32-bit shared atomics instead of a 64-bit one
+            uint32_t* cx = reinterpret_cast<uint32_t*>(&S.capx[lib]);
+            atomicXor(cx, (uint32_t)x);
+            atomicXor(cx + 1, (uint32_t)(x >> 32));
+        }
     }
     __syncwarp();
     // NA: mover stones whose group has >= 2 liberties (this row's X runs)
@@ -351,7 +343,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
             int cell = r * N + p;
             h2 = h ^ __ldg(zX + cell);
             if ((capb >> p) & 1u) h2 ^= S.capx[cell];
-            S.hit[lane] = h2;
+            S.u.hit[lane] = h2;
         }
         __syncwarp();
         unsigned found = 0u;
@@ -359,7 +351,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
             uint64_t v = j < nscan ? hist[j] : extra;
             for (unsigned a_ = active; a_; a_ &= a_ - 1) {
                 int l = __ffs(a_) - 1;
-                if (v == S.hit[l]) found |= 1u << l;
+                if (v == S.u.hit[l]) found |= 1u << l;
             }
         }
         found = __reduce_or_sync(BBK_FULL, found);
@@ -430,6 +422,26 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
 
     for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
+        if (!p.force_reset && b + nwarps < p.n) {
+            // Warm L2 with the NEXT board's inputs (14 lines of pat + Bloom, 10 scalar columns) so
+            // its loads hit L2 instead of HBM; costs no shared memory.
+            const int64_t nb = b + nwarps;
+            const char* ptr = nullptr;
+            if (lane < 6) ptr = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS) + 128 * lane;
+            else if (lane < 14) ptr = reinterpret_cast<const char*>(p.store.bloom + nb * (int64_t)BBK_GO_BLOOM_WORDS) +
+                                      128 * (lane - 6);
+            else if (lane == 14) ptr = reinterpret_cast<const char*>(p.in.terminated + nb);
+            else if (lane == 15) ptr = reinterpret_cast<const char*>(p.in.truncated + nb);
+            else if (lane == 16) ptr = reinterpret_cast<const char*>(p.in.step_count + nb);
+            else if (lane == 17) ptr = reinterpret_cast<const char*>(p.in.player_to_role + 2 * nb);
+            else if (lane == 18) ptr = reinterpret_cast<const char*>(p.in_s.role_to_move + nb);
+            else if (lane == 19) ptr = reinterpret_cast<const char*>(p.in_s.pass_count + nb);
+            else if (lane == 20) ptr = reinterpret_cast<const char*>(p.in_s.hash + nb);
+            else if (lane == 21) ptr = reinterpret_cast<const char*>(p.in_s.hist_xor + nb);
+            else if (lane == 22) ptr = reinterpret_cast<const char*>(p.in_s.hist_len + nb);
+            else if (lane == 23) ptr = reinterpret_cast<const char*>(p.actions + nb);
+            if (ptr) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+        }
         const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
@@ -528,13 +540,13 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             role = 1 - role;
         }
         // new transposed history: pat' = pat << 2 | current board (go.py:224, 260)
-        if (lane < 32) { S.rowB[lane] = Bk; S.rowW[lane] = Wh; }
+        S.rX[lane] = Bk; S.rY[lane] = Wh;   // rowB / rowW for the pat update
         __syncwarp();
         uint16_t* opat = p.out_s.pat + b * (int64_t)PS;
         if (!reset) {
             for (int i = lane; i < C; i += 32) {
                 int rr = i / N, cc = i - rr * N;
-                uint32_t v = ((uint32_t)S.pat[i] << 2) | ((S.rowB[rr] >> cc) & 1u) | (((S.rowW[rr] >> cc) & 1u) << 1);
+                uint32_t v = ((uint32_t)S.pat[i] << 2) | ((S.rX[rr] >> cc) & 1u) | (((S.rY[rr] >> cc) & 1u) << 1);
                 S.pat[i] = (uint16_t)v;
             }
         }
@@ -550,15 +562,17 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             legal = legal_rows<N>(S, zob_table<N>() + role * C, zob_table<N>() + (1 - role) * C, X, Y, E, h, hist, nscan,
                                   extra, lane);
         }
+        __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit
         const int64_t mstart = b * (int64_t)A;
         const int moff = (int)(mstart & 15);
         if (lane < N) {
-            for (int col = 0; col < N; col++) S.mb[moff + lane * N + col] = (uint8_t)((legal >> col) & 1u);
+            for (int col = 0; col < N; col++) S.u.mb[moff + lane * N + col] = (uint8_t)((legal >> col) & 1u);
         }
-        if (lane == 0) S.mb[moff + C] = (uint8_t)(!terminal && !truncated);
+        if (lane == 0) S.u.mb[moff + C] = (uint8_t)(!terminal && !truncated);
         __syncwarp();
-        warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.mb);
+        warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.u.mb);
+        __syncwarp();   // staged mask bytes are overwritten by the observation pattern next
         if (p.out.observation) emit_obs<N>(S, B.lut, p.out.observation, b, role, lane);
         if (lane == 0) {
             float r0 = 0.0f, r1 = 0.0f;
