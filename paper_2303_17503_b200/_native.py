@@ -11,7 +11,7 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libbbk.so")
+LIB_PATH = os.environ.get("BBK_LIB") or os.path.join(_PKG, "_lib", "libbbk.so")   # BBK_LIB: A/B builds
 
 _lock = threading.Lock()
 _lib = None
@@ -93,7 +93,7 @@ def lib():
             return _lib
         from . import build as _build
         try:
-            if _build.needs_build():
+            if not os.environ.get("BBK_LIB") and _build.needs_build():
                 _build.build()
         except Exception as exc:  # nvcc missing or compile error
             if not os.path.exists(LIB_PATH):

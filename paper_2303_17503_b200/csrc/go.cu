@@ -58,7 +58,10 @@ struct WarpSmem {
         } uf;
         uint64_t hit[32];
         alignas(16) uint8_t mb[((A + 47) & ~15)];
-        uint32_t P[C + 4];
+        struct {
+            uint32_t P[C + 4];
+            uint32_t W[(C * 17 + 31) / 32 + 2];
+        } ob;
     } u;
     alignas(16) uint16_t pat[pat_stride(N)];
     uint32_t rX[32], rY[32], rSX[32], rSY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
@@ -365,34 +368,37 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
 }
 
 // Observation of one board from the transposed history in S.pat (new
-// state), colour plane = role (go.py:264-273). Flat-stream emission.
+// state), colour plane = role (go.py:264-273). Float f of the record is bit
+// f % 17 of the point pattern P[f / 17]; the [N, N, 17] record is emitted as
+// float4 chunks of the flat 16-byte-aligned stream (records are not 16-B
+// aligned; at most 3 scalar floats at each edge) through a 16-entry LUT.
 template <int N>
 __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t b, int role, int lane) {
     constexpr int C = N * N;
     constexpr int NF = C * kPlanes;
+    uint32_t* P = S.u.ob.P;
     for (int i = lane; i < C; i += 32) {
         uint32_t v = S.pat[i];
         if (role) v = ((v & 0x5555u) << 1) | ((v >> 1) & 0x5555u);
-        S.u.P[i] = v | ((uint32_t)role << 16);
+        P[i] = v | ((uint32_t)role << 16);
     }
-    if (lane < 4) S.u.P[C + lane] = 0u;
+    if (lane < 4) P[C + lane] = 0u;
     __syncwarp();
     const int64_t F0 = b * (int64_t)NF;
-    const int64_t a0 = (F0 + 3) & ~(int64_t)3, a1 = (F0 + NF) & ~(int64_t)3;
-    if (lane < 8) {   // scalar head (<=3 floats) and tail (<=3 floats)
-        int64_t f = lane < 4 ? F0 + lane : a1 + (lane - 4);
-        bool ok = lane < 4 ? f < a0 : f < F0 + NF;
-        if (ok) {
-            uint32_t fi = (uint32_t)(f - F0);
-            uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;
-            obs[f] = (float)((S.u.P[c] >> k) & 1u);
-        }
+    const int head = (int)((4 - (F0 & 3)) & 3);             // floats before the first aligned chunk
+    const int nchunk = (NF - head) >> 2;
+    float* rec = obs + F0;
+    const int tail0 = head + 4 * nchunk;
+    if (lane < head || (lane >= 4 && lane - 4 < NF - tail0)) {
+        const uint32_t fi = lane < 4 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 4);
+        const uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;
+        rec[fi] = (float)((P[c] >> k) & 1u);
     }
-    float4* o4 = reinterpret_cast<float4*>(obs);
-    for (int64_t j = (a0 >> 2) + lane; j < (a1 >> 2); j += 32) {
-        uint32_t fi = (uint32_t)((j << 2) - F0);
-        uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;   // fi/17, exact for fi < 65536
-        uint64_t w = (uint64_t)S.u.P[c] | ((uint64_t)S.u.P[c + 1] << 17);
+    float4* o4 = reinterpret_cast<float4*>(rec + head);
+    for (int j = lane; j < nchunk; j += 32) {
+        const uint32_t fi = (uint32_t)(head + 4 * j);
+        const uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;   // fi / 17, exact for fi < 65536
+        const uint64_t w = (uint64_t)P[c] | ((uint64_t)P[c + 1] << 17);
         o4[j] = lut[(uint32_t)(w >> k) & 15u];
     }
     __syncwarp();
