@@ -51,7 +51,7 @@ struct WarpSmem {
     union {
         struct {
             uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
-            uint16_t par[MAXR];    // union-find over run indices
+            uint32_t par[MAXR];    // union-find over run indices
             uint32_t gst[MAXR];    // OR(lib) | OR(~lib) << 10 | HAS, at group roots
             uint16_t root[MAXR];
             uint8_t atari[MAXR];
@@ -99,6 +99,12 @@ template <int N>
 __device__ __forceinline__ const uint64_t* zob_table() {
     return g_zob.v[N == 9 ? 0 : N == 13 ? 1 : 2];
 }
+// zobrist key of (cell, colour) computed in registers: with shared memory taking
+// most of the unified L1, a table lookup would be an L2 round trip; mix64 is ~15 ALU ops.
+template <int N>
+__device__ __forceinline__ uint64_t zkey(int cell, int colour) {
+    return mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)cell + (uint64_t)colour);
+}
 
 template <int N>
 struct BlockSmem {
@@ -134,25 +140,24 @@ __device__ __forceinline__ uint32_t uf_find(volatile uint32_t* par, uint32_t x) 
 
 // find with path halving; racing lanes only ever re-point a node at one of its
 // ancestors, so the forest stays valid while other lanes hook roots with CAS.
-__device__ __forceinline__ uint32_t uf_find_halve(volatile uint16_t* par, uint32_t x) {
+__device__ __forceinline__ uint32_t uf_find_halve(volatile uint32_t* par, uint32_t x) {
     while (true) {
         const uint32_t p = par[x];
         if (p == x) return x;
         const uint32_t gp = par[p];
-        if (gp != p) par[x] = (uint16_t)gp;
+        if (gp != p) par[x] = gp;
         x = gp;
     }
 }
 
-__device__ __forceinline__ void uf_union(uint16_t* par, uint32_t a, uint32_t b) {
-    volatile uint16_t* vp = par;
+__device__ __forceinline__ void uf_union(uint32_t* par, uint32_t a, uint32_t b) {
+    volatile uint32_t* vp = par;
     while (true) {
         a = uf_find_halve(vp, a);
         b = uf_find_halve(vp, b);
         if (a == b) return;
         if (a < b) { uint32_t t = a; a = b; b = t; }
-        const uint32_t old = atomicCAS(reinterpret_cast<unsigned short*>(&par[a]), (unsigned short)a,
-                                       (unsigned short)b);
+        const uint32_t old = atomicCAS(&par[a], a, b);
         if (old == a) return;
     }
 }
@@ -215,8 +220,8 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 }
 
 // Legal mask rows for the side to move (go.py:121-174, allow_self_capture
-// off). X = mover's stones, Y = opponent's stones, E = empties (row bits of
-// this lane). `zX`/`zY` are the zobrist tables of the two colours.
+// off). X = mover's stones, Y = opponent's stones (colour index `ycol`),
+// E = empties (row bits of this lane).
 //
 // Group analysis (go.py:45-80 restated for what the mask needs): every
 // horizontal run of stones is a union-find node. Runs are laid out as a flat
@@ -224,7 +229,7 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 // liberty / classification passes stride lanes over RUNS, not rows -- the work
 // is balanced no matter how the stones are distributed over the rows.
 template <int N>
-__device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_t* zY, uint32_t X, uint32_t Y,
+__device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
                                uint32_t E, uint64_t h, const uint64_t* hist, int nscan, uint64_t extra, int lane) {
     constexpr uint32_t ROW = (1u << N) - 1u;
     auto& U = S.u.uf;
@@ -253,7 +258,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
             U.run[k] = (uint16_t)((1u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(Y >> s)) - 1));
         }
     }
-    for (int i = lane; i < total; i += 32) { U.par[i] = (uint16_t)i; U.gst[i] = 0u; }
+    for (int i = lane; i < total; i += 32) { U.par[i] = (uint32_t)i; U.gst[i] = 0u; }
     for (int i = lane; i < (N * N + 1) / 2; i += 32)
         reinterpret_cast<uint4*>(S.capx)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
@@ -282,7 +287,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
             const uint32_t p = U.par[x];
             if (p == x) break;
             const uint32_t gp = U.par[p];
-            U.par[x] = (uint16_t)gp;
+            U.par[x] = gp;
             x = gp;
         }
         U.root[i] = (uint16_t)x;
@@ -308,7 +313,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
             atomicOr(&S.rcap[lib / N], 1u << (lib % N));
             const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
             uint64_t x = 0ull;
-            for (int q = 0; q < len; q++) x ^= __ldg(zY + rr * N + s + q);
+            for (int q = 0; q < len; q++) x ^= zkey<N>(rr * N + s + q, ycol);
             // XOR is bitwise: two native 32-bit shared atomics instead of a 64-bit one
             uint32_t* cx = reinterpret_cast<uint32_t*>(&S.capx[lib]);
             atomicXor(cx, (uint32_t)x);
@@ -333,7 +338,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
     for (uint32_t c_ = cand; c_; c_ &= c_ - 1) {
         int p = __ffs(c_) - 1;
         int cell = r * N + p;
-        uint64_t h2 = h ^ __ldg(zX + cell);
+        uint64_t h2 = h ^ zkey<N>(cell, 1 - ycol);
         if ((capb >> p) & 1u) h2 ^= S.capx[cell];
         if (bloom_maybe(S.bloom, h2)) pend |= 1u << p;
         else legal |= 1u << p;
@@ -344,7 +349,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, const uint64_t* zX, const uint64_
         uint64_t h2 = 0ull;
         if (pend) {
             int cell = r * N + p;
-            h2 = h ^ __ldg(zX + cell);
+            h2 = h ^ zkey<N>(cell, 1 - ycol);
             if ((capb >> p) & 1u) h2 ^= S.capx[cell];
             S.u.hit[lane] = h2;
         }
@@ -504,8 +509,6 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                 uint32_t M = role == 0 ? Bk : Wh, O = role == 0 ? Wh : Bk;
                 if (lane == ra) M |= 1u << ca;
                 const uint32_t E0 = ~(M | O) & rowm;
-                const uint64_t* zM = zob_table<N>() + role * C;
-                const uint64_t* zO = zob_table<N>() + (1 - role) * C;
                 uint64_t capxor = 0ull;
                 uint32_t visited = 0u, dead = 0u;
                 const int qr_[4] = {ra - 1, ra + 1, ra, ra};
@@ -532,9 +535,9 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                     visited |= F;
                     if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E0) != 0u)) dead |= F;
                 }
-                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= __ldg(zO + lane * N + __ffs(d_) - 1);
+                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zkey<N>(lane * N + __ffs(d_) - 1, 1 - role);
                 O &= ~dead;
-                const uint64_t h2 = h ^ __ldg(zM + a) ^ warp_xor64(capxor);
+                const uint64_t h2 = h ^ zkey<N>(a, role) ^ warp_xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
                 if (lane == 0) {
                     hist[hlen] = h2;
@@ -565,8 +568,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            legal = legal_rows<N>(S, zob_table<N>() + role * C, zob_table<N>() + (1 - role) * C, X, Y, E, h, hist, nscan,
-                                  extra, lane);
+            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, nscan, extra, lane);
         }
         __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit

@@ -21,9 +21,10 @@ for r in rows:
         continue
     k = (cur_file, int(r[0]))
     src[k] = r[1].strip()
-    agg[k] += int(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0)
-    inst[k] += int(r[hdr.index("Instructions Executed")] or 0)
-    thr[k] += int(r[hdr.index("Thread Instructions Executed")] or 0)
+    num = lambda x: int(x) if x.strip().lstrip("-").isdigit() else 0
+    agg[k] += num(r[hdr.index("Warp Stall Sampling (All Samples)")])
+    inst[k] += num(r[hdr.index("Instructions Executed")])
+    thr[k] += num(r[hdr.index("Thread Instructions Executed")])
 tot, ti = sum(agg.values()), sum(inst.values())
 print(f"samples {tot}  warp-instructions {ti}  lane-eff {sum(thr.values()) / max(ti, 1):.1f}")
 for k, v in agg.most_common(top):
