@@ -45,6 +45,7 @@ struct WarpSmem {
     uint8_t prep[8];
     uint64_t pinray[8];
     int8_t pinsq[8];
+    uint16_t task[2][136];             // (piece, ray) work units: own [0], opponent [1]
 };
 
 struct Params {
@@ -123,133 +124,162 @@ __device__ __forceinline__ int action_of(int fl, int from, int to, int promo) {
     return f * 73 + plane;
 }
 
-struct MoveCtx {
-    const uint8_t* bd;
-    uint8_t* mask;
-    int side, fl, ksq;
-    uint64_t att;        // opponent attacks with our king removed
-    uint64_t checkmask;  // legal destinations for non-king moves
-    const int8_t* pinsq;
-    const uint64_t* pinray;
-    int ep;
-};
+// ------------------------------------------------------------ task lists
+// Work is distributed over (piece, ray) TASKS instead of squares: a slider
+// contributes one task per direction, a knight / king / pawn one task. All 32
+// lanes then stride over the task list, so the (few, uneven) pieces do not
+// serialise the warp. Task = square | dir << 6 (dir 8 = whole piece).
+__device__ __constant__ int8_t FLIPD[8] = {4, 3, 2, 1, 0, 7, 6, 5};   // vertical flip of a queen direction
+__device__ __constant__ int8_t FLIPK[8] = {3, 2, 1, 0, 7, 6, 5, 4};   // vertical flip of a knight jump
 
-__device__ __forceinline__ uint64_t pin_of(const MoveCtx& c, int s) {
-    uint64_t r = ~0ull;
-#pragma unroll
-    for (int d = 0; d < 8; d++) if (c.pinsq[d] == s) r = c.pinray[d];
-    return r;
+__device__ __forceinline__ int ntasks_of(uint8_t pc) {
+    const int t = pc & 7;
+    return !pc ? 0 : t == Q ? 8 : (t == R || t == B) ? 4 : 1;
 }
 
-// Emit the legal moves of our piece on `s`; returns (count, ep_legal).
-__device__ int gen_square(const MoveCtx& c, int s, bool& ep_legal) {
-    const uint8_t pc = c.bd[s];
-    if (!pc || color(pc) != c.side) return 0;
-    const int t = type(pc), r = s >> 3, f = s & 7, side = c.side;
+// Build both task lists (own = `side`, opponent) with one packed warp scan.
+__device__ void build_tasks(const uint8_t* bd, int side, uint16_t (*task)[136], int& n_own, int& n_opp, int lane) {
+    const uint8_t p0 = bd[lane], p1 = bd[lane + 32];
+    const int o0 = (p0 && color(p0) == side) ? ntasks_of(p0) : 0, o1 = (p1 && color(p1) == side) ? ntasks_of(p1) : 0;
+    const int x0 = (p0 && color(p0) != side) ? ntasks_of(p0) : 0, x1 = (p1 && color(p1) != side) ? ntasks_of(p1) : 0;
+    const int mine = (o0 + o1) | ((x0 + x1) << 16);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(BBK_FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int tot = __shfl_sync(BBK_FULL, incl, 31);
+    n_own = tot & 0xFFFF; n_opp = tot >> 16;
+    int ko = (incl - mine) & 0xFFFF, kx = (incl - mine) >> 16;
+    auto put = [&](uint16_t* list, int& k, int sq, uint8_t pc, int n) {
+        const int t = pc & 7;
+        if (n == 1) { list[k++] = (uint16_t)(sq | (8 << 6)); return; }
+        const int d0 = t == B ? 1 : 0, stp = t == Q ? 1 : 2;
+        for (int d = d0; d < 8; d += stp) list[k++] = (uint16_t)(sq | (d << 6));
+    };
+    if (o0) put(task[0], ko, lane, p0, o0);
+    if (o1) put(task[0], ko, lane + 32, p1, o1);
+    if (x0) put(task[1], kx, lane, p0, x0);
+    if (x1) put(task[1], kx, lane + 32, p1, x1);
+}
+
+// Attack bits of one opponent task (our king `ksq` is transparent to sliders).
+__device__ __forceinline__ uint64_t task_attacks(const uint8_t* bd, uint16_t tk, int ksq) {
+    const int sq = tk & 63, d = tk >> 6, r = sq >> 3, f = sq & 7;
+    const uint8_t pc = bd[sq];
+    const int t = type(pc), by = color(pc);
+    uint64_t a = 0ull;
+    if (d < 8) {
+        int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+        while (on(rr, ff)) {
+            const int to = rr * 8 + ff;
+            a |= 1ull << to;
+            if (bd[to] && to != ksq) break;
+            rr += DIR_DR[d]; ff += DIR_DF[d];
+        }
+    } else if (t == N) {
+        for (int k = 0; k < 8; k++) { int rr = r + KN_DR[k], ff = f + KN_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+    } else if (t == K) {
+        for (int k = 0; k < 8; k++) { int rr = r + DIR_DR[k], ff = f + DIR_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+    } else {   // pawn
+        const int rr = by == 0 ? r + 1 : r - 1;
+        if (on(rr, f - 1)) a |= 1ull << (rr * 8 + f - 1);
+        if (on(rr, f + 1)) a |= 1ull << (rr * 8 + f + 1);
+    }
+    return a;
+}
+
+struct GenCtx {
+    const uint8_t* bd;
+    uint8_t* mask;
+    int side, fl, ksq, ep;
+    uint64_t att, checkmask;
+    const int8_t* pinsq;
+    const uint64_t* pinray;
+};
+
+// Emit the legal moves of one own task into the staged mask; returns the count.
+__device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
+    const int sq = tk & 63, d = tk >> 6, r = sq >> 3, f = sq & 7;
+    const uint8_t pc = c.bd[sq];
+    const int t = type(pc), side = c.side;
+    const int from = (sq ^ c.fl) * 73;
     int cnt = 0;
     if (t == K) {
-        for (int d = 0; d < 8; d++) {
-            int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+        for (int k = 0; k < 8; k++) {
+            const int rr = r + DIR_DR[k], ff = f + DIR_DF[k];
             if (!on(rr, ff)) continue;
-            int to = rr * 8 + ff;
-            uint8_t q = c.bd[to];
-            if (q && color(q) == side) continue;
-            if ((c.att >> to) & 1ull) continue;
-            c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
-        }
-        return cnt;   // castling handled by the caller (needs rights)
-    }
-    const uint64_t allow = c.checkmask & pin_of(c, s);
-    if (t == P) {
-        const int dr = side == 0 ? 1 : -1, last = side == 0 ? 7 : 0, start = side == 0 ? 1 : 6;
-        const int r1 = r + dr;
-        if (!on(r1, f)) return 0;
-        auto emit = [&](int to) {
-            if (r1 == last) {
-                c.mask[action_of(c.fl, s, to, Q)] = 1;
-                c.mask[action_of(c.fl, s, to, R)] = 1;
-                c.mask[action_of(c.fl, s, to, B)] = 1;
-                c.mask[action_of(c.fl, s, to, N)] = 1;
-                cnt += 4;
-            } else {
-                c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
-            }
-        };
-        const int to1 = r1 * 8 + f;
-        if (!c.bd[to1]) {
-            if ((allow >> to1) & 1ull) emit(to1);
-            const int to2 = (r + 2 * dr) * 8 + f;
-            if (r == start && !c.bd[to2] && ((allow >> to2) & 1ull)) emit(to2);
-        }
-        for (int df = -1; df <= 1; df += 2) {
-            if (!on(r1, f + df)) continue;
-            const int to = r1 * 8 + f + df;
+            const int to = rr * 8 + ff;
             const uint8_t q = c.bd[to];
-            if (q && color(q) != side) {
-                if ((allow >> to) & 1ull) emit(to);
-            } else if (to == c.ep) {
-                const int cap = side == 0 ? to - 8 : to + 8;
-                if (!attacked_mod(c.bd, c.ksq, 1 - side, s, cap, to, pc)) {
-                    c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
-                    ep_legal = true;
-                }
-            }
+            if ((q && color(q) == side) || ((c.att >> to) & 1ull)) continue;
+            c.mask[from + (c.fl ? FLIPD[k] : k) * 7] = 1; cnt++;
+        }
+        return cnt;
+    }
+    uint64_t allow = c.checkmask;
+#pragma unroll
+    for (int j = 0; j < 8; j++) if (c.pinsq[j] == sq) allow &= c.pinray[j];
+    if (d < 8) {   // slider ray
+        const int dm = (c.fl ? FLIPD[d] : d) * 7;
+        int rr = r + DIR_DR[d], ff = f + DIR_DF[d], k = 0;
+        while (on(rr, ff)) {
+            const int to = rr * 8 + ff;
+            const uint8_t q = c.bd[to];
+            if (q && color(q) == side) break;
+            if ((allow >> to) & 1ull) { c.mask[from + dm + k] = 1; cnt++; }
+            if (q) break;
+            rr += DIR_DR[d]; ff += DIR_DF[d]; k++;
         }
         return cnt;
     }
     if (t == N) {
         for (int k = 0; k < 8; k++) {
-            int rr = r + KN_DR[k], ff = f + KN_DF[k];
+            const int rr = r + KN_DR[k], ff = f + KN_DF[k];
             if (!on(rr, ff)) continue;
-            int to = rr * 8 + ff;
-            uint8_t q = c.bd[to];
+            const int to = rr * 8 + ff;
+            const uint8_t q = c.bd[to];
             if ((q && color(q) == side) || !((allow >> to) & 1ull)) continue;
-            c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++;
+            c.mask[from + 56 + (c.fl ? FLIPK[k] : k)] = 1; cnt++;
         }
         return cnt;
     }
-    const int d0 = t == B ? 1 : 0, stp = (t == B || t == R) ? 2 : 1;
-    for (int d = d0; d < 8; d += stp) {
-        int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
-        while (on(rr, ff)) {
-            int to = rr * 8 + ff;
-            uint8_t q = c.bd[to];
-            if (q && color(q) == side) break;
-            if ((allow >> to) & 1ull) { c.mask[action_of(c.fl, s, to, 0)] = 1; cnt++; }
-            if (q) break;
-            rr += DIR_DR[d]; ff += DIR_DF[d];
+    // pawn (mover frame: forward = N, captures NW / NE)
+    const int dr = side == 0 ? 1 : -1, last = side == 0 ? 7 : 0, start = side == 0 ? 1 : 6;
+    const int r1 = r + dr;
+    auto emit = [&](int to, int df, int plane_q) {
+        if (r1 == last) {
+            c.mask[from + plane_q] = 1;                       // queen promotion = queen-move plane
+            c.mask[from + 64 + 0 * 3 + df + 1] = 1;           // N, B, R under-promotions
+            c.mask[from + 64 + 1 * 3 + df + 1] = 1;
+            c.mask[from + 64 + 2 * 3 + df + 1] = 1;
+            cnt += 4;
+        } else {
+            c.mask[from + plane_q] = 1; cnt++;
         }
+    };
+    const int to1 = r1 * 8 + f;
+    if (!c.bd[to1]) {
+        if ((allow >> to1) & 1ull) emit(to1, 0, 0 * 7 + 0);
+        const int to2 = (r + 2 * dr) * 8 + f;
+        if (r == start && !c.bd[to2] && ((allow >> to2) & 1ull)) emit(to2, 0, 0 * 7 + 1);
     }
-    return cnt;
-}
-
-// Attacks of the opponent piece on `s` (king `ksq` transparent to sliders).
-__device__ uint64_t attacks_from(const uint8_t* bd, int s, int by, int ksq) {
-    const uint8_t pc = bd[s];
-    if (!pc || color(pc) != by) return 0ull;
-    const int t = type(pc), r = s >> 3, f = s & 7;
-    uint64_t a = 0ull;
-    if (t == P) {
-        int rr = by == 0 ? r + 1 : r - 1;
-        if (on(rr, f - 1)) a |= 1ull << (rr * 8 + f - 1);
-        if (on(rr, f + 1)) a |= 1ull << (rr * 8 + f + 1);
-    } else if (t == N) {
-        for (int k = 0; k < 8; k++) { int rr = r + KN_DR[k], ff = f + KN_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
-    } else if (t == K) {
-        for (int d = 0; d < 8; d++) { int rr = r + DIR_DR[d], ff = f + DIR_DF[d]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
-    } else {
-        const int d0 = t == B ? 1 : 0, stp = (t == B || t == R) ? 2 : 1;
-        for (int d = d0; d < 8; d += stp) {
-            int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
-            while (on(rr, ff)) {
-                int to = rr * 8 + ff;
-                a |= 1ull << to;
-                if (bd[to] && to != ksq) break;
-                rr += DIR_DR[d]; ff += DIR_DF[d];
+    for (int df = -1; df <= 1; df += 2) {
+        if (!on(r1, f + df)) continue;
+        const int to = r1 * 8 + f + df;
+        const uint8_t q = c.bd[to];
+        const int plane = (df < 0 ? 7 : 1) * 7;               // NW / NE, distance 1
+        if (q && color(q) != side) {
+            if ((allow >> to) & 1ull) emit(to, df, plane);
+        } else if (to == c.ep) {
+            const int cap = side == 0 ? to - 8 : to + 8;
+            if (!attacked_mod(c.bd, c.ksq, 1 - side, sq, cap, to, pc)) {
+                c.mask[from + plane] = 1; cnt++;
+                ep_legal = true;
             }
         }
     }
-    return a;
+    return cnt;
 }
 
 // Apply a move encoded in the mover's frame (mirrors oracle make()).
@@ -290,7 +320,7 @@ __device__ __forceinline__ void load_past(uint8_t* dst, const uint8_t* hist_env,
     dst[2 * lane + 1] = byte >> 4;
 }
 
-__global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
+__global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
@@ -338,7 +368,12 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
         const unsigned kb0 = __ballot_sync(BBK_FULL, S.bd[lane] == mk(side, K));
         const unsigned kb1 = __ballot_sync(BBK_FULL, S.bd[lane + 32] == mk(side, K));
         const int ksq = kb0 ? __ffs(kb0) - 1 : kb1 ? 32 + __ffs(kb1) - 1 : 0;
-        const uint64_t att = warp_or64(attacks_from(S.bd, lane, opp, ksq) | attacks_from(S.bd, lane + 32, opp, ksq));
+        int n_own, n_opp;
+        build_tasks(S.bd, side, S.task, n_own, n_opp, lane);
+        __syncwarp();
+        uint64_t att_l = 0ull;
+        for (int i = lane; i < n_opp; i += 32) att_l |= task_attacks(S.bd, S.task[1][i], ksq);
+        const uint64_t att = warp_or64(att_l);
         const bool in_check = (att >> ksq) & 1ull;
         bool checker = false;
         uint64_t block = 0ull;
@@ -379,12 +414,13 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
         const int nchecks = __popc(__ballot_sync(BBK_FULL, checker));
         const uint64_t blockall = warp_or64(block);
         __syncwarp();
-        MoveCtx c;
-        c.bd = S.bd; c.mask = S.mask; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att;
+        GenCtx c;
+        c.bd = S.bd; c.mask = S.mask; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
         c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
-        c.pinsq = S.pinsq; c.pinray = S.pinray; c.ep = ep;
+        c.pinsq = S.pinsq; c.pinray = S.pinray;
         bool ep_legal = false;
-        int cnt = gen_square(c, lane, ep_legal) + gen_square(c, lane + 32, ep_legal);
+        int cnt = 0;
+        for (int i = lane; i < n_own; i += 32) cnt += task_moves(c, S.task[0][i], ep_legal);
         if (lane == 0 && !in_check) {   // castling (oracle gen_pseudo castling rules)
             const int rank = side == 0 ? 0 : 56, kbit = side == 0 ? 1 : 4, qbit = side == 0 ? 2 : 8;
             if (ksq == rank + 4) {
