@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="add a batch-size sweep 2^10..2^17 to the line")
+    ap.add_argument("--unfused", action="store_true", help="separate sampler / step / counter launches")
     return ap.parse_args()
 
 
@@ -141,25 +142,36 @@ def run_gpu(args, rank, world, local):
     root = bb.RngKey(args.seed)
     slot0 = rank * B   # global slot index: bit-identical to one big batch
 
-    # ping-pong device states: only the previous batch stays valid in bench mode
-    cur = kern.init(gdef, root.child(0), B, limit, slot0=slot0, device=dev)
-    spare = kern.new_v(B, slot0, dev, 0, limit)
-    acts = torch.empty(B, dtype=torch.int64, device=dev)
+    # ping-pong device states: only the previous batch stays valid in bench mode.
+    # Fused loop (default): each step kernel also samples the NEXT step's random actions from
+    # the new legal mask (agents.random_actions with the schedule's key) and counts finished
+    # slots, so one step = one launch. --unfused runs sampler / step / counter as 3 launches.
+    acts = [torch.empty(B, dtype=torch.int64, device=dev) for _ in range(2)]
     episodes = torch.zeros(1, dtype=torch.int64, device=dev)
+    cur = kern.init(gdef, root.child(0), B, limit, slot0=slot0, device=dev,
+                    next_key=None if args.unfused else root.child(1), next_actions=acts[0])
+    spare = kern.new_v(B, slot0, dev, 0, limit)
     lib = __import__("paper_2303_17503_b200._native", fromlist=["lib"]).lib()
     stream = torch.cuda.current_stream(dev)
     t = 0
 
     def one_step(ev=None):
         nonlocal cur, spare, t
-        kern.random_actions(cur, root.child(2 * t + 1), out=acts)
+        a_now, a_next = acts[t % 2], acts[(t + 1) % 2]
+        if args.unfused:
+            kern.random_actions(cur, root.child(2 * t + 1), out=a_now)
         if ev is not None:
             ev[0].record(stream)
-        nxt = kern.step(gdef, cur, acts, root.child(2 * (t + 1)), limit, validate=False, out=spare)
+        if args.unfused:
+            nxt = kern.step(gdef, cur, a_now, root.child(2 * (t + 1)), limit, validate=False, out=spare)
+        else:
+            nxt = kern.step(gdef, cur, a_now, root.child(2 * (t + 1)), limit, validate=False, out=spare,
+                            next_key=root.child(2 * (t + 1) + 1), next_actions=a_next, episodes=episodes)
         if ev is not None:
             ev[1].record(stream)
-        lib.bbk_count_finished(nxt.dev.terminated.data_ptr(), nxt.dev.truncated.data_ptr(), B,
-                               episodes.data_ptr(), stream.cuda_stream)
+        if args.unfused:
+            lib.bbk_count_finished(nxt.dev.terminated.data_ptr(), nxt.dev.truncated.data_ptr(), B,
+                                   episodes.data_ptr(), stream.cuda_stream)
         spare, cur = cur, nxt
         t += 1
 
@@ -215,7 +227,7 @@ def run_gpu(args, rank, world, local):
                        gdef.spec.observation_shape) / 1e9),
                    "timed": "K steps after W warm-up steps from init (step t of the BatchSession schedule)"},
         "clocks": clk,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (3 if args.unfused else 1) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                      "kernel": STEP_KERNEL[game], "kernel_ms": avg_kern_ms,
@@ -247,10 +259,11 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     """
     import torch
 
+    from paper_2303_17503_b200.agents import random_actions_device
     from paper_2303_17503_b200.core import Batch, batch_step
 
     batch = Batch(gdef, B, gdef.max_steps, vstate=kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0,
-                                                            device=dev))
+                                                            device=dev, next_key=root.child(1)))
     host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
     host_r = torch.empty((B, 2), dtype=torch.float32, pin_memory=True)
     host_f = torch.empty((B, 2), dtype=torch.uint8, pin_memory=True)
@@ -259,9 +272,10 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
 
     def one():
         nonlocal batch, t
-        a = kern.random_actions(batch._v, root.child(2 * t + 1))
+        a = random_actions_device(batch, root.child(2 * t + 1))   # fused: produced by the previous launch
         host_act.copy_(a)
-        batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False)
+        batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False,
+                           next_key=root.child(2 * (t + 1) + 1))
         d = batch.device
         host_r.copy_(d.rewards, non_blocking=True)
         host_f[:, 0].copy_(d.terminated, non_blocking=True)
@@ -302,9 +316,10 @@ def run_sweep(args, gdef, kern, dev, slot0):
         B = 1 << e
         if gdef.game_id == "shogi" and e > 16:
             continue
-        cur = kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0, device=dev)
+        acts = [torch.empty(B, dtype=torch.int64, device=dev) for _ in range(2)]
+        cur = kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0, device=dev, next_key=root.child(1),
+                        next_actions=acts[0])
         spare = kern.new_v(B, slot0, dev, 0, gdef.max_steps)
-        acts = torch.empty(B, dtype=torch.int64, device=dev)
         n_steps = 64
         t = 0
         for k in range(8 + n_steps):
@@ -312,8 +327,8 @@ def run_sweep(args, gdef, kern, dev, slot0):
                 torch.cuda.synchronize()
                 s, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
-            kern.random_actions(cur, root.child(2 * t + 1), out=acts)
-            nxt = kern.step(gdef, cur, acts, root.child(2 * (t + 1)), gdef.max_steps, validate=False, out=spare)
+            nxt = kern.step(gdef, cur, acts[t % 2], root.child(2 * (t + 1)), gdef.max_steps, validate=False, out=spare,
+                            next_key=root.child(2 * (t + 1) + 1), next_actions=acts[(t + 1) % 2])
             spare, cur = cur, nxt
             t += 1
         e_.record()

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define BBK_ABI_VERSION 1
+#define BBK_ABI_VERSION 2
 
 typedef struct bbk_cols {
     float*    observation;        /* may be NULL: skip observation emission */
@@ -45,6 +45,14 @@ typedef struct bbk_cols {
     int32_t*  current_player;
     int32_t*  step_count;
     int8_t*   player_to_role;
+    /* Optional fused outputs of an init/step call (ignored in `in` columns):
+     *   next_actions[n]  agents.random_actions(new batch, next_key) (agents.py:33-46),
+     *                    sampled from the new legal mask while it is still on chip,
+     *                    so the benchmark loop needs no separate sampling pass;
+     *   episodes         += number of finished slots (bench.py:129). */
+    int64_t*  next_actions;
+    uint64_t  next_key;
+    unsigned long long* episodes;
 } bbk_cols;
 
 /* ------------------------------------------------------------------ Go --

@@ -33,7 +33,8 @@ I32 = C.c_int32
 
 class Cols(C.Structure):
     _fields_ = [("observation", P), ("legal_action_mask", P), ("rewards", P), ("terminated", P),
-                ("truncated", P), ("current_player", P), ("step_count", P), ("player_to_role", P)]
+                ("truncated", P), ("current_player", P), ("step_count", P), ("player_to_role", P),
+                ("next_actions", P), ("next_key", U64), ("episodes", P)]
 
 
 class GoState(C.Structure):

@@ -23,6 +23,8 @@ def random_actions_device(batch, key: RngKey, out=None):
     finished slots get 0 (agents.py:33-46), computed by bbk_random_actions.
     """
     v = batch._v
+    if out is None and v.next_actions is not None and v.next_key == key.state:
+        return v.next_actions   # already sampled by the fused step/init kernel from the same mask and key
     return v.kern.random_actions(v, key, out)
 
 

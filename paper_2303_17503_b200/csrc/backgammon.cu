@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
     WarpSmem& S = sm[threadIdx.x >> 5];
     const int lane = lane_id();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    unsigned long long eps = 0;
     for (int64_t base = ((int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5)) * 32; base < p.n; base += nwarps * 32) {
         const int64_t b = base + lane;
         const bool live = b < p.n;
@@ -203,6 +204,25 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
             }
             truncated = !s.terminal && step >= p.max_steps;
             if (!s.terminal && !truncated) legal_mask(s, m);
+            eps += (s.terminal || truncated) ? 1 : 0;
+            if (p.out.next_actions) {   // fused agents.random_actions on the new mask
+                const int count = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]) + __popc(m[4]);
+                int64_t act = 0;
+                if (count > 0) {
+                    int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)count);
+                    for (int j = 0; j < 5; j++) {
+                        const int pc = __popc(m[j]);
+                        if (d < pc) {
+                            uint32_t v = m[j];
+                            for (; d > 0; d--) v &= v - 1;
+                            act = 32 * j + __ffs(v) - 1;
+                            break;
+                        }
+                        d -= pc;
+                    }
+                }
+                p.out.next_actions[b] = act;
+            }
             store_board(s, p.out_s, b);
             float r0 = 0.0f, r1 = 0.0f;
             if (!truncated && (s.rr0 != 0.0f || s.rr1 != 0.0f)) {
@@ -226,6 +246,10 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
             warp_emit_bytes(reinterpret_cast<uint8_t*>(p.out.observation), base * OBS * 4, (int)(cnt * OBS * 4),
                             reinterpret_cast<const uint8_t*>(S.ob));
         __syncwarp();
+    }
+    if (p.out.episodes) {
+        const int e = warp_sum((int)eps);
+        if (lane == 0 && e) atomicAdd(p.out.episodes, (unsigned long long)e);
     }
 }
 

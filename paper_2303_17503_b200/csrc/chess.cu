@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
     WarpSmem& S = sm[threadIdx.x >> 5];
     const int lane = lane_id();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    unsigned long long eps = 0;
     for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
         const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
@@ -485,6 +486,12 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             terminal = true;
         }
         const bool truncated = !terminal && step >= p.max_steps;
+        eps += (terminal || truncated) ? 1 : 0;
+        if (p.out.next_actions) {   // fused agents.random_actions on the new mask (still in shared memory)
+            const int64_t a = warp_sample_bytes(S.mask, A, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
+                                                p.slot0 + b);
+            if (lane == 0) p.out.next_actions[b] = a;
+        }
         // ---- history entry for this ply, then the past boards for the observation
         if (lane < 2) reinterpret_cast<uint4*>(hist + (step & (RING - 1)) * 32)[lane] =
             reinterpret_cast<const uint4*>(S.packed)[lane];
@@ -576,6 +583,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         }
         __syncwarp();
     }
+    if (p.out.episodes && lane_id() == 0 && eps) atomicAdd(p.out.episodes, eps);
 }
 
 // observe(state, player) for an explicit role: rebuild from board + history.

@@ -79,3 +79,57 @@ __device__ __forceinline__ void warp_emit_bytes(uint8_t* dst_stream, int64_t rec
 }
 
 }  // namespace bbk
+
+namespace bbk {
+
+// agents.random_actions (reference agents.py:33-46) for ONE slot whose legal
+// mask is staged in shared memory as 0/1 bytes at mask[0..A): returns the
+// index of the d-th legal action, d = child(key, slot) % max(count, 1), or 0.
+// Warp-cooperative: lanes count contiguous word ranges, scan, and the lane
+// holding the d-th set byte resolves it. `mask` may be unaligned.
+__device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A, int count, uint64_t key,
+                                                     int64_t slot) {
+    if (count <= 0) return 0;
+    const int lane = lane_id();
+    const int d = (int)(child(key, (uint64_t)slot) % (uint64_t)count);
+    const uintptr_t base = reinterpret_cast<uintptr_t>(mask);
+    const int head = (int)(base & 3);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(base - head);
+    const int nw = (head + A + 3) >> 2;
+    const int per = (nw + 31) >> 5;
+    const int w0 = lane * per, w1 = min(w0 + per, nw);
+    auto word_at = [&](int i) -> uint32_t {
+        uint32_t v = w[i] & 0x01010101u;
+        const int b0 = 4 * i - head;                     // row byte of the word's byte 0
+        if (b0 < 0) v &= 0xFFFFFFFFu << (8 * (-b0));
+        if (b0 + 4 > A) v &= 0xFFFFFFFFu >> (8 * (b0 + 4 - A));
+        return v;
+    };
+    int c = 0;
+    for (int i = w0; i < w1; i++) c += __popc(word_at(i));
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(BBK_FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int excl = incl - c;
+    int64_t act = -1;
+    if (d >= excl && d < incl) {
+        int r = d - excl;
+        for (int i = w0; i < w1; i++) {
+            uint32_t v = word_at(i);
+            const int pc = __popc(v);
+            if (r < pc) {
+                for (; r > 0; r--) v &= v - 1;
+                act = 4 * i + ((__ffs(v) - 1) >> 3) - head;
+                break;
+            }
+            r -= pc;
+        }
+    }
+    const unsigned who = __ballot_sync(BBK_FULL, act >= 0);
+    return __shfl_sync(BBK_FULL, act, __ffs(who) - 1);
+}
+
+}  // namespace bbk

@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
     WarpSmem<N>& S = B.w[threadIdx.x >> 5];
     const uint32_t rowm = lane < N ? ROW : 0u;
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    unsigned long long eps = 0;
 
     for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
         if (!p.force_reset && b + nwarps < p.n) {
@@ -580,6 +581,36 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
         if (lane == 0) S.u.mb[moff + C] = (uint8_t)(!terminal && !truncated);
         __syncwarp();
         warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.u.mb);
+        eps += (terminal || truncated) ? 1 : 0;
+        if (p.out.next_actions) {   // fused agents.random_actions on the new mask (row bits + pass, still on chip)
+            const int c = __popc(legal);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(BBK_FULL, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int cells = __shfl_sync(BBK_FULL, incl, 31);
+            const bool live = !terminal && !truncated;
+            const int total = live ? cells + 1 : 0;   // + pass
+            int64_t act = 0;
+            if (total > 0) {
+                const int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)total);
+                if (d == cells) act = C;
+                else {
+                    const bool mine = d >= incl - c && d < incl;
+                    int pos = 0;
+                    if (mine) {
+                        uint32_t v = legal;
+                        for (int r = d - (incl - c); r > 0; r--) v &= v - 1;
+                        pos = lane * N + __ffs(v) - 1;
+                    }
+                    const unsigned who = __ballot_sync(BBK_FULL, mine);
+                    act = __shfl_sync(BBK_FULL, pos, __ffs(who) - 1);
+                }
+            }
+            if (lane == 0) p.out.next_actions[b] = act;
+        }
         __syncwarp();   // staged mask bytes are overwritten by the observation pattern next
         if (p.out.observation) emit_obs<N>(S, B.lut, p.out.observation, b, role, lane);
         if (lane == 0) {
@@ -604,6 +635,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
         }
         __syncwarp();
     }
+    if (p.out.episodes && lane == 0 && eps) atomicAdd(p.out.episodes, eps);
 }
 
 template <int N>

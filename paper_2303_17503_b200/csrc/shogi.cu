@@ -254,7 +254,7 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
+__global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
     const int lane = lane_id();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     const int cap = p.out_s.hist_cap;
+    unsigned long long eps = 0;
     for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
         const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
@@ -535,6 +536,12 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
             terminal = true;
         }
         const bool truncated = !terminal && step >= p.max_steps;
+        eps += (terminal || truncated) ? 1 : 0;
+        if (p.out.next_actions) {   // fused agents.random_actions on the new mask (still in shared memory)
+            const int64_t a = warp_sample_bytes(mk, A, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
+                                                p.slot0 + b);
+            if (lane == 0) p.out.next_actions[b] = a;
+        }
         build_and_emit_obs(S, lut, hand, side, in_check, p.out.observation, b, lane);
         // ---- mask emission (flat byte stream; records are not 16-B aligned)
         __syncwarp();
@@ -560,8 +567,8 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
         }
         __syncwarp();
     }
+    if (p.out.episodes && lane_id() == 0 && eps) atomicAdd(p.out.episodes, eps);
 }
-
 
 // observe(state, player) for an explicit role per slot (no history planes in shogi).
 __global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st, const uint8_t* role, float* obs,

@@ -55,11 +55,12 @@ class Env:
     def init(self, key, batch_size: int | None = None) -> State:
         root = key if isinstance(key, RngKey) else RngKey(int(key))
         n = self.batch_size if batch_size is None else batch_size
-        return State(batch_init(self.gdef, root.child(0), n, max_steps=self.max_steps), root, 0)
+        return State(batch_init(self.gdef, root.child(0), n, max_steps=self.max_steps, next_key=root.child(1)), root, 0)
 
     def step(self, state: State, action, key: RngKey | None = None, validate: bool = True) -> State:
         k = key if key is not None else state._root.child(2 * (state._t + 1))
-        return State(batch_step(state._batch, action, k, validate=validate), state._root, state._t + 1)
+        nk = state._root.child(2 * (state._t + 1) + 1)
+        return State(batch_step(state._batch, action, k, validate=validate, next_key=nk), state._root, state._t + 1)
 
     def random_action(self, state: State):
         from .agents import random_actions_device

@@ -89,6 +89,8 @@ class DeviceV:
         self.store = None
         self.uid = _next_uid()
         self._host = {}
+        self.next_actions = None     # fused agents.random_actions output of the producing call
+        self.next_key = None
 
     # lazily materialised host columns (the reference reads them via getattr)
     def _h(self, name):
@@ -145,11 +147,14 @@ class DeviceKernel:
         raise NotImplementedError
 
     @staticmethod
-    def cols(v: DeviceV) -> nat.Cols:
+    def cols(v: DeviceV, fused: tuple | None = None) -> nat.Cols:
+        """Column pointers; `fused` = (next_key_state, next_actions tensor, episodes tensor) or None."""
         d = v.dev
+        nk, na, ep = fused if fused is not None else (0, None, None)
         return nat.Cols(nat.ptr(d.observation), nat.ptr(d.legal_action_mask), nat.ptr(d.rewards),
                         nat.ptr(d.terminated), nat.ptr(d.truncated), nat.ptr(d.current_player),
-                        nat.ptr(d.step_count), nat.ptr(d.player_to_role))
+                        nat.ptr(d.step_count), nat.ptr(d.player_to_role), nat.ptr(na), int(nk) & ((1 << 64) - 1),
+                        nat.ptr(ep))
 
     @staticmethod
     def _device(device):
@@ -170,13 +175,33 @@ class DeviceKernel:
 
     # -------------------------------------------------------- protocol: init
     def init(self, gdef, key, n: int, limit: int, slot_keys=None, slot0: int = 0, device=None,
-             obs: bool = True) -> DeviceV:
+             obs: bool = True, next_key=None, next_actions=None, episodes=None) -> DeviceV:
         device = self._device(device)
         v = self.new_v(n, slot0, device, 0, limit, obs)
         sk = self._slot_keys(slot_keys, device)
         ks = 0 if key is None else key_state(key)
-        self.launch_init(v, ks, sk)
+        self._fused = self._fused_args(v, next_key, next_actions, episodes)
+        try:
+            self.launch_init(v, ks, sk)
+        finally:
+            self._fused = None
         return v
+
+    def _fused_args(self, v, next_key, next_actions, episodes):
+        """Optional fused outputs of a launch (bbk_cols.next_actions / next_key / episodes)."""
+        if next_key is None and episodes is None:
+            return None
+        torch = _torch()
+        if next_key is not None and next_actions is None:
+            next_actions = torch.empty(v.n, dtype=torch.int64, device=v.device)
+        if next_key is not None:
+            v.next_actions = next_actions
+            v.next_key = key_state(next_key)
+        return (0 if next_key is None else key_state(next_key), next_actions if next_key is not None else None,
+                episodes)
+
+    def out_cols(self, v: DeviceV) -> nat.Cols:
+        return self.cols(v, getattr(self, "_fused", None))
 
     # -------------------------------------------------------- protocol: step
     def as_actions(self, actions, v: DeviceV):
@@ -206,7 +231,7 @@ class DeviceKernel:
             raise IllegalAction(f"slot {slot}: illegal action {act} in {self.game_id}", action=act, slot=slot)
 
     def step(self, gdef, v: DeviceV, actions, key, limit: int, validate: bool = True, slot_keys=None,
-             out: DeviceV | None = None) -> DeviceV:
+             out: DeviceV | None = None, next_key=None, next_actions=None, episodes=None) -> DeviceV:
         a = self.as_actions(actions, v)
         if validate:
             self.validate(v, a)
@@ -219,8 +244,14 @@ class DeviceKernel:
             out.limit = limit
             out.uid = _next_uid()
             out._host = {}
+            out.next_actions = None
+            out.next_key = None
         self.prepare_step(v, out)
-        self.launch_step(v, out, a, ks, sk, limit)
+        self._fused = self._fused_args(out, next_key, next_actions, episodes)
+        try:
+            self.launch_step(v, out, a, ks, sk, limit)
+        finally:
+            self._fused = None
         return out
 
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:

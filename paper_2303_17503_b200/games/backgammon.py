@@ -54,11 +54,11 @@ class BackgammonKernel(DeviceKernel):
         return nat.BgState(nat.ptr(v.priv.points[i:i + 1]), nat.ptr(v.priv.misc[i:i + 1]))
 
     def launch_init(self, v, ks, sk):
-        nat.check(nat.lib().bbk_bg_init(self.cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
+        nat.check(nat.lib().bbk_bg_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_bg_init")
 
     def launch_step(self, v, out, a, ks, sk, limit):
-        nat.check(nat.lib().bbk_bg_step(self.cols(v), self.state_struct(v), self.cols(out), self.state_struct(out),
+        nat.check(nat.lib().bbk_bg_step(self.cols(v), self.state_struct(v), self.out_cols(out), self.state_struct(out),
                                         nat.ptr(a), v.n, v.slot0, ks, nat.ptr(sk), limit,
                                         nat.stream_handle(v.device)), "bbk_bg_step")
 

@@ -74,7 +74,7 @@ class RingKernel(DeviceKernel):
         v.store = RingStore(torch.empty((v.n, self.hist_bytes), dtype=torch.uint8, device=v.device))
         v.store.lineage = Lineage(v.uid)
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_init")
-        nat.check(fn(self.cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
+        nat.check(fn(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                      nat.stream_handle(v.device)), f"bbk_{self.prefix}_init")
 
     def prepare_step(self, v, out):
@@ -88,7 +88,7 @@ class RingKernel(DeviceKernel):
 
     def launch_step(self, v, out, a, ks, sk, limit):
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_step")
-        nat.check(fn(self.cols(v), self.state_struct(v), self.cols(out), self.state_struct(out), nat.ptr(a), v.n,
+        nat.check(fn(self.cols(v), self.state_struct(v), self.out_cols(out), self.state_struct(out), nat.ptr(a), v.n,
                      v.slot0, ks, nat.ptr(sk), limit, nat.stream_handle(v.device)), f"bbk_{self.prefix}_step")
 
     def launch_observe(self, v, i, roles, out):

@@ -108,7 +108,7 @@ class GoKernel(DeviceKernel):
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
         v.store = self.new_store(v.n, v.limit, v.device)
         v.store.lineage = Lineage(v.uid)
-        cols, st, store = self.cols(v), self.state_struct(v), v.store.struct()
+        cols, st, store = self.out_cols(v), self.state_struct(v), v.store.struct()
         nat.check(nat.lib().bbk_go_init(self.size, cols, st, store, v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_go_init")
 
@@ -131,7 +131,7 @@ class GoKernel(DeviceKernel):
         store.lineage.advance(v.uid, out.uid)
 
     def launch_step(self, v, out, a, ks, sk, limit) -> None:
-        nat.check(nat.lib().bbk_go_step(self.size, self.komi, self.cols(v), self.state_struct(v), self.cols(out),
+        nat.check(nat.lib().bbk_go_step(self.size, self.komi, self.cols(v), self.state_struct(v), self.out_cols(out),
                                         self.state_struct(out), out.store.struct(), nat.ptr(a), v.n, v.slot0, ks,
                                         nat.ptr(sk), limit, nat.stream_handle(v.device)), "bbk_go_step")
 

@@ -55,7 +55,7 @@ class ShogiKernel(RingKernel):
         torch = _torch()
         v.store = RingStore(torch.empty((v.n, int(v.limit) + 2), dtype=torch.int64, device=v.device))
         v.store.lineage = Lineage(v.uid)
-        nat.check(nat.lib().bbk_shogi_init(self.cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
+        nat.check(nat.lib().bbk_shogi_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                            nat.stream_handle(v.device)), "bbk_shogi_init")
 
     def prepare_step(self, v, out):

@@ -26,7 +26,8 @@ class BatchSession:
         self.root = RngKey(seed)
         self.workers = workers
         self.validate = validate
-        self.batch: Batch = batch_init(self.gdef, self.root.child(0), batch_size, max_steps=max_steps)
+        self.batch: Batch = batch_init(self.gdef, self.root.child(0), batch_size, max_steps=max_steps,
+                                       next_key=self.root.child(1))
         self.t = 0
 
     def sample_random_actions(self):
@@ -34,7 +35,8 @@ class BatchSession:
         return random_actions_device(self.batch, self.root.child(2 * self.t + 1))
 
     def step(self, actions) -> Batch:
-        batch = batch_step(self.batch, actions, self.root.child(2 * (self.t + 1)), validate=self.validate)
+        batch = batch_step(self.batch, actions, self.root.child(2 * (self.t + 1)), validate=self.validate,
+                           next_key=self.root.child(2 * (self.t + 1) + 1))
         self.t += 1
         self.batch = batch
         return batch

@@ -176,3 +176,25 @@ def test_slot_sharding_is_bit_identical():
     for r in range(parts):
         for name in ("observation", "legal_action_mask", "rewards", "current_player"):
             assert torch.equal(getattr(shards[r].dev, name), getattr(full.dev, name)[r * 16:(r + 1) * 16]), name
+
+
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"])
+def test_fused_sampling_and_episode_counter(game):
+    """Step kernels that also sample the next random actions equal the separate sampler kernel."""
+    import torch
+    from paper_2303_17503_b200.core import resolve
+
+    gdef = resolve(game)
+    kern = gdef.batch_kernel
+    n = 96
+    root = bb.RngKey(21)
+    eps = torch.zeros(1, dtype=torch.int64, device="cuda")
+    v = kern.init(gdef, root.child(0), n, gdef.max_steps, next_key=root.child(1))
+    total = 0
+    for t in range(60):
+        ref = kern.random_actions(v, root.child(2 * t + 1), out=torch.empty(n, dtype=torch.int64, device="cuda"))
+        assert torch.equal(v.next_actions, ref), t
+        v = kern.step(gdef, v, v.next_actions, root.child(2 * (t + 1)), gdef.max_steps, validate=False,
+                      next_key=root.child(2 * (t + 1) + 1), episodes=eps)
+        total += int((v.dev.terminated | v.dev.truncated).sum())
+    assert int(eps.item()) == total
