@@ -62,20 +62,16 @@ __device__ __forceinline__ void warp_emit_bytes(uint8_t* dst_stream, int64_t rec
                                                 const uint8_t* staged /* 16B aligned, data at +off */) {
     const int lane = lane_id();
     const int64_t end = rec_start + nbytes;
-    const int64_t c0 = rec_start >> 4;            // first chunk (may be partial)
-    const int64_t c1 = (end + 15) >> 4;           // one past last chunk
-    for (int64_t c = c0 + lane; c < c1; c += 32) {
-        const int64_t g0 = c << 4;
-        const uint8_t* s = staged + (g0 - (rec_start & ~(int64_t)15));
-        if (g0 >= rec_start && g0 + 16 <= end) {
-            *reinterpret_cast<uint4*>(dst_stream + g0) = *reinterpret_cast<const uint4*>(s);
-        } else {
-            for (int k = 0; k < 16; k++) {
-                int64_t g = g0 + k;
-                if (g >= rec_start && g < end) dst_stream[g] = s[k];
-            }
-        }
-    }
+    const int64_t base = rec_start & ~(int64_t)15;
+    const int64_t f0 = (rec_start + 15) >> 4;     // first full chunk
+    const int64_t f1 = end >> 4;                  // one past the last full chunk
+    for (int64_t c = f0 + lane; c < f1; c += 32)
+        *reinterpret_cast<uint4*>(dst_stream + (c << 4)) = *reinterpret_cast<const uint4*>(staged + ((c << 4) - base));
+    // edge bytes: lanes 0-15 the partial head chunk, lanes 16-31 the partial tail chunk
+    const int64_t head_end = (f0 << 4) < end ? (f0 << 4) : end;
+    const int64_t g = lane < 16 ? rec_start + lane : (f1 << 4) + (lane - 16);
+    const bool ok = lane < 16 ? g < head_end : (g < end && g >= (f0 << 4));
+    if (ok) dst_stream[g] = staged[g - base];
 }
 
 }  // namespace bbk

@@ -28,6 +28,7 @@ constexpr int NF = 81 * 119;        // 9639 floats per record
 constexpr int kWarps = 4;
 constexpr int BOARD_STRIDE = 96;
 constexpr int MISC = 16;            // hand[2][7], stm, rep
+constexpr int BLOOM_U64 = 32;       // 2048-bit repetition Bloom filter after each env's key log
 
 enum { EMP = 0, FU = 1, KY, KE, GI, KI, KA, HI, OU, TO, NY, NK, NG, UM, RY };
 
@@ -189,20 +190,25 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
     // ---- observation bitstream
     for (int i = lane; i < NF / 32 + 4; i += 32) S.bits[i] = 0u;
     __syncwarp();
-    uint32_t cpat[4] = {0u, 0u, 0u, 0u};   // constant planes 62..118 (hands, check)
-    {
-        for (int who = 0; who < 2; who++) {
-            const int own_side = who == 0 ? side : 1 - side;
-            for (int hi = 0; hi < 7; hi++) {
-                const int cntp = hand[own_side * 7 + hi] < HCAP[hi] ? hand[own_side * 7 + hi] : HCAP[hi];
-                for (int q = 0; q < cntp; q++) {
-                    const int bit = 62 + 28 * who + HOFF[hi] + q;
-                    cpat[bit >> 5] |= 1u << (bit & 31);
-                }
-            }
+    // constant planes 62..118 (hand thresholds, check) as a 64-bit word at bit 62:
+    // hand type hi of player `who` sets min(count, cap) ones at 28*who + HOFF[hi]
+    uint64_t hp = 0ull;
+#pragma unroll
+    for (int who = 0; who < 2; who++) {
+        const int own_side = who == 0 ? side : 1 - side;
+#pragma unroll
+        for (int hi = 0; hi < 7; hi++) {
+            const uint32_t c = hand[own_side * 7 + hi], cap = HCAP[hi];
+            const uint32_t n = c < cap ? c : cap;
+            hp |= (uint64_t)((1u << n) - 1u) << (28 * who + HOFF[hi]);
         }
-        if (in_check) cpat[118 >> 5] |= 1u << (118 & 31);
     }
+    if (in_check) hp |= 1ull << (118 - 62);
+    uint32_t cpat[4];   // bits 62..118 of a 128-bit record pattern
+    cpat[0] = 0u;
+    cpat[1] = (uint32_t)(hp << 30);            // bits 62,63
+    cpat[2] = (uint32_t)(hp >> 2);
+    cpat[3] = (uint32_t)(hp >> 34);
     for (int pass = 0; pass < 4; pass++) {
         const int s = pass < 2 ? 2 * lane + pass : 64 + 2 * lane + (pass - 2);
         if (s < 81) {
@@ -233,23 +239,20 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
         }
         __syncwarp();
     }
-    if (obs_stream) {
-        float* obs = obs_stream;
+    if (obs_stream) {   // flat [n, 9, 9, 119] stream; records are not 16-B aligned
         const int64_t F0 = b * (int64_t)NF;
-        const int64_t a0 = (F0 + 3) & ~(int64_t)3, a1 = (F0 + NF) & ~(int64_t)3;
-        if (lane < 8) {
-            const int64_t f = lane < 4 ? F0 + lane : a1 + (lane - 4);
-            const bool ok = lane < 4 ? f < a0 : f < F0 + NF;
-            if (ok) {
-                const uint32_t fi = (uint32_t)(f - F0);
-                obs[f] = (float)((S.bits[fi >> 5] >> (fi & 31)) & 1u);
-            }
+        const int head = (int)((4 - (F0 & 3)) & 3);
+        const int nchunk = (NF - head) >> 2;
+        const int tail0 = head + 4 * nchunk;
+        float* rec = obs_stream + F0;
+        if (lane < head || (lane >= 4 && lane - 4 < NF - tail0)) {
+            const uint32_t fi = lane < 4 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 4);
+            rec[fi] = (float)((S.bits[fi >> 5] >> (fi & 31)) & 1u);
         }
-        float4* o4 = reinterpret_cast<float4*>(obs);
-        for (int64_t j = (a0 >> 2) + lane; j < (a1 >> 2); j += 32) {
-            const uint32_t fi = (uint32_t)((j << 2) - F0);
-            const uint64_t w2 = (uint64_t)S.bits[fi >> 5] | ((uint64_t)S.bits[(fi >> 5) + 1] << 32);
-            o4[j] = lut[(uint32_t)(w2 >> (fi & 31)) & 15u];
+        float4* o4 = reinterpret_cast<float4*>(rec + head);
+        for (int j = lane; j < nchunk; j += 32) {
+            const uint32_t fi = (uint32_t)(head + 4 * j);
+            o4[j] = lut[__funnelshift_r(S.bits[fi >> 5], S.bits[(fi >> 5) + 1], fi & 31) & 15u];
         }
     }
 }
@@ -378,9 +381,17 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
             if (son(tr, tc)) {
                 const int t = tr * 9 + tc;
                 const uint8_t q = bd[t];
-                if (!(q && owner(q) == 0)) {
-                    Acc at{bd, ksq, t, -1, 0, OU, 0};
-                    ok = !attacked(at, t, 1);
+                if (!(q && owner(q) == 0) && S.acnt[1][t] == 0) {
+                    // the gather saw every attacker except a slider x-raying through our king:
+                    // walk once from the king away from t
+                    const int od = OPPD[d];
+                    int xr = kr + DR[od], xc = kc + DC[od];
+                    ok = true;
+                    while (son(xr, xc)) {
+                        const uint8_t pc = bd[xr * 9 + xc];
+                        if (pc) { ok = !(owner(pc) == 1 && ((SLIDE[ptype(pc)] >> od) & 1)); break; }
+                        xr += DR[od]; xc += DC[od];
+                    }
                 }
             }
             S.kesc[d] = ok;
@@ -523,10 +534,25 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
         }
         key = warp_xor64(key);
         if (side) key ^= mix64(0x5306300000000000ULL);
+        // four-fold repetition: 2048-bit Bloom filter of the ply log (stored after it), exact
+        // scan of the log only on a Bloom hit (identical answers to scanning every key)
+        uint32_t* bloom = reinterpret_cast<uint32_t*>(hist + cap - BLOOM_U64);
+        const uint32_t i1 = (uint32_t)key & 2047u, i2 = (uint32_t)(key >> 11) & 2047u;
+        if (step == 0) {
+            for (int j = lane; j < 2 * BLOOM_U64; j += 32) bloom[j] = 0u;
+            __syncwarp();
+        }
         int reps = 0;
-        for (int j = lane; j < step; j += 32) reps += hist[j] == key;
-        reps = warp_sum(reps);
-        if (lane == 0) hist[step] = key;
+        if (step > 0 && ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & 1u)) {
+            for (int j = lane; j < step; j += 32) reps += hist[j] == key;
+            reps = warp_sum(reps);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            hist[step] = key;
+            atomicOr(&bloom[i1 >> 5], 1u << (i1 & 31));
+            atomicOr(&bloom[i2 >> 5], 1u << (i2 & 31));
+        }
         bool terminal = false;
         float rr0 = 0.0f, rr1 = 0.0f;
         if (nlegal == 0) {   // no legal move: the side to move loses

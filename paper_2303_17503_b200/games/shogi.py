@@ -53,13 +53,14 @@ class ShogiKernel(RingKernel):
 
     def launch_init(self, v, ks, sk):
         torch = _torch()
-        v.store = RingStore(torch.empty((v.n, int(v.limit) + 2), dtype=torch.int64, device=v.device))
+        # per env: position keys by ply (max_steps + 2) then a 2048-bit repetition Bloom filter (32 x u64)
+        v.store = RingStore(torch.empty((v.n, int(v.limit) + 2 + 32), dtype=torch.int64, device=v.device))
         v.store.lineage = Lineage(v.uid)
         nat.check(nat.lib().bbk_shogi_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                            nat.stream_handle(v.device)), "bbk_shogi_init")
 
     def prepare_step(self, v, out):
-        if out.limit + 2 > v.store.hist.shape[1]:
+        if out.limit + 2 + 32 > v.store.hist.shape[1]:
             raise ValueError("max_steps exceeds the position-log capacity of this batch")
         super().prepare_step(v, out)
 
