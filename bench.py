@@ -64,6 +64,19 @@ def dist_env():
     return rank, world, local
 
 
+def ncu_traffic(game: str, B: int):
+    """DRAM bytes per step-kernel launch from the committed ncu --set full capture (profiles/)."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")
+        try:
+            with open(path) as fh:
+                d = json.load(fh)[game]
+            return d["dram_bytes_per_env_step"] * B, f"profiles/{rnd}/ncu_traffic.json ({d['captured']})"
+        except Exception:
+            continue
+    return None, None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -207,6 +220,7 @@ def run_gpu(args, rank, world, local):
     avg_kern_ms = sum(kern_ms) / len(kern_ms)
     peak, peak_kind = peaks()
     achieved = B_ALG[game] * B / (avg_kern_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(game, B)
     out = {
         "metric": METRIC,
         "value": value,
@@ -229,7 +243,8 @@ def run_gpu(args, rank, world, local):
         "clocks": clk,
         "gpu_launches": (3 if args.unfused else 1) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_kind,
                      "kernel": STEP_KERNEL[game], "kernel_ms": avg_kern_ms,
                      "kernel_share_of_step": avg_kern_ms / (ms / args.steps),
                      "bytes_per_env_step": B_ALG[game]},
