@@ -43,28 +43,31 @@ template <int N>
 struct WarpSmem {
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
-    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
-    uint32_t bloom[BBK_GO_BLOOM_WORDS];
+    // >= max runs of both colours, and >= the Bloom filter's 256 words (it reuses `par`)
+    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32 > 256 ? ((N + 1) / 2) * 2 * N + 32 : 256;
     uint64_t capx[C];
     // Phase-multiplexed scratch (each member is dead before the next one is written):
     // group analysis -> superko hits -> staged mask bytes -> observation pattern.
     union {
         struct {
+            uint32_t par[MAXR];    // union-find over run indices; then the env's Bloom filter (cp.async)
             uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
-            uint32_t par[MAXR];    // union-find over run indices
             uint32_t gst[MAXR];    // OR(lib) | OR(~lib) << 10 | HAS, at group roots
             uint16_t root[MAXR];
-            uint8_t atari[MAXR];
         } uf;
-        uint64_t hit[32];
+        struct {
+            uint32_t bloom_area[BBK_GO_BLOOM_WORDS];
+            uint64_t hit[32];
+        } sk;
         alignas(16) uint8_t mb[((A + 47) & ~15)];
         struct {
             uint32_t P[C + 4];
             uint32_t W[(C * 17 + 31) / 32 + 2];
         } ob;
     } u;
+    static_assert(MAXR * 4 >= BBK_GO_BLOOM_WORDS * 4, "parent array must hold the Bloom filter");
     alignas(16) uint16_t pat[pat_stride(N)];
-    uint32_t rX[32], rY[32], rSX[32], rSY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
+    uint32_t rX[32], rY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
     int32_t roff[33];
 };
 
@@ -169,16 +172,12 @@ __device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
     return ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & (bloom[i3 >> 5] >> (i3 & 31)) & 1u) != 0;
 }
 
-// Lane 0 only: add h to both the shared copy and the env's global filter.
-__device__ __forceinline__ void bloom_add(uint32_t* sb, uint32_t* gb, uint64_t h) {
-    uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
-                       (uint32_t)(h >> 26) & (kBloomBits - 1)};
+// Lane 0 only: add h to the env's global filter.
+__device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
+    const uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
+                             (uint32_t)(h >> 26) & (kBloomBits - 1)};
 #pragma unroll
-    for (int j = 0; j < 3; j++) {
-        uint32_t w = idx[j] >> 5;
-        sb[w] |= 1u << (idx[j] & 31);
-        if (gb) gb[w] = sb[w];
-    }
+    for (int j = 0; j < 3; j++) gb[idx[j] >> 5] |= 1u << (idx[j] & 31);
 }
 
 __device__ __forceinline__ uint32_t up_row(uint32_t v, int lane) {
@@ -229,8 +228,8 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 // liberty / classification passes stride lanes over RUNS, not rows -- the work
 // is balanced no matter how the stones are distributed over the rows.
 template <int N>
-__device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
-                               uint32_t E, uint64_t h, const uint64_t* hist, int nscan, uint64_t extra, int lane) {
+__device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y, uint32_t E, uint64_t h,
+                               const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra, int lane) {
     constexpr uint32_t ROW = (1u << N) - 1u;
     auto& U = S.u.uf;
     const int r = lane;
@@ -244,7 +243,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     }
     const int total = __shfl_sync(BBK_FULL, off, 31);
     off -= cnt;
-    S.rX[lane] = X; S.rY[lane] = Y; S.rSX[lane] = SX; S.rSY[lane] = SY; S.rE[lane] = E; S.rcap[lane] = 0u;
+    S.rX[lane] = X; S.rY[lane] = Y; S.rE[lane] = E; S.rcap[lane] = 0u;
     S.roff[lane] = off;
     if (lane == 31) S.roff[32] = total;
     {   // this row's runs -> list
@@ -269,8 +268,8 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         if (rr == 0) continue;
         const int col = e >> 15, s = (e >> 5) & 31, len = e & 31;
         const uint32_t Zu = col ? S.rY[rr - 1] : S.rX[rr - 1];
-        const uint32_t Su = col ? S.rSY[rr - 1] : S.rSX[rr - 1];
-        const int base = S.roff[rr - 1] + (col ? __popc(S.rSX[rr - 1]) : 0);
+        const uint32_t Su = Zu & ~(Zu << 1);   // run starts of the row above
+        const int base = S.roff[rr - 1] + (col ? __popc(S.rX[rr - 1] & ~(S.rX[rr - 1] << 1)) : 0);
         uint32_t V = (((1u << len) - 1u) << s) & Zu;
         while (V) {
             const int c = __ffs(V) - 1;
@@ -302,11 +301,21 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         atomicOr(&U.gst[x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
     __syncwarp();
+    // the parent array is dead now: async-copy this env's 1 KB Bloom filter into it, overlapped
+    // with the classification pass (it includes the hash appended by this step)
+    const uint32_t* bl = U.par;
+    {
+        __threadfence_block();
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.par) + 16u * lane;
+        const char* src = reinterpret_cast<const char*>(gbloom) + 16 * lane;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 512u), "l"(src + 512));
+        asm volatile("cp.async.commit_group;");
+    }
     // 3. atari classification; capture liberties (+ zobrist XOR) of opponent atari groups
     for (int i = lane; i < total; i += 32) {
         const uint32_t g = U.gst[U.root[i]];
         const bool at = !(g & 0x80000000u) || (g & (g >> 10) & 0x3FFu) == 0u;
-        U.atari[i] = at;
         const uint32_t e = U.run[i];
         if ((e >> 15) && at && (g & 0x80000000u)) {
             const uint32_t lib = g & 0x3FFu;
@@ -320,13 +329,17 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
             atomicXor(cx + 1, (uint32_t)(x >> 32));
         }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     // NA: mover stones whose group has >= 2 liberties (this row's X runs)
     uint32_t NA = 0u;
     {
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++)
-            if (!U.atari[k]) NA |= run_at(X, __ffs(s_) - 1);
+        {
+            const uint32_t g = U.gst[U.root[k]];
+            if ((g & (g >> 10) & 0x3FFu) != 0u) NA |= run_at(X, __ffs(s_) - 1);   // >= 2 liberties
+        }
     }
     // 5. candidates + superko filter (row-parallel)
     const uint32_t Eu = up_row(E, lane), Ed = dn_row(E, lane);
@@ -340,7 +353,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         int cell = r * N + p;
         uint64_t h2 = h ^ zkey<N>(cell, 1 - ycol);
         if ((capb >> p) & 1u) h2 ^= S.capx[cell];
-        if (bloom_maybe(S.bloom, h2)) pend |= 1u << p;
+        if (bloom_maybe(bl, h2)) pend |= 1u << p;
         else legal |= 1u << p;
     }
     while (__any_sync(BBK_FULL, pend != 0u)) {
@@ -351,7 +364,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
             int cell = r * N + p;
             h2 = h ^ zkey<N>(cell, 1 - ycol);
             if ((capb >> p) & 1u) h2 ^= S.capx[cell];
-            S.u.hit[lane] = h2;
+            S.u.sk.hit[lane] = h2;
         }
         __syncwarp();
         unsigned found = 0u;
@@ -359,7 +372,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
             uint64_t v = j < nscan ? hist[j] : extra;
             for (unsigned a_ = active; a_; a_ &= a_ - 1) {
                 int l = __ffs(a_) - 1;
-                if (v == S.u.hit[l]) found |= 1u << l;
+                if (v == S.u.sk.hit[l]) found |= 1u << l;
             }
         }
         found = __reduce_or_sync(BBK_FULL, found);
@@ -472,11 +485,10 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
             role = 0; pass_count = 0; step = 0; h = 0ull; hx = 0ull; hlen = 1;
             for (int i = lane; i < PS; i += 32) S.pat[i] = 0;
-            for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) S.bloom[i] = 0u;
+            for (int i = lane; i < BBK_GO_BLOOM_WORDS / 4; i += 32)
+                reinterpret_cast<uint4*>(gbloom)[i] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
-            if (lane == 0) { bloom_add(S.bloom, nullptr, 0ull); hist[0] = 0ull; }
-            __syncwarp();
-            for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) gbloom[i] = S.bloom[i];
+            if (lane == 0) { bloom_add(gbloom, 0ull); hist[0] = 0ull; }
             nscan = 0; extra = 0ull;
         } else {
             p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
@@ -485,8 +497,6 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             h = p.in_s.hash[b]; hx = p.in_s.hist_xor[b]; hlen = p.in_s.hist_len[b];
             const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
             for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
-            const uint4* gb4 = reinterpret_cast<const uint4*>(gbloom);
-            for (int i = lane; i < BBK_GO_BLOOM_WORDS / 4; i += 32) reinterpret_cast<uint4*>(S.bloom)[i] = gb4[i];
             __syncwarp();
             if (lane < N) {
 #pragma unroll 4
@@ -542,7 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
                 if (lane == 0) {
                     hist[hlen] = h2;
-                    bloom_add(S.bloom, gbloom, h2);
+                    bloom_add(gbloom, h2);
                 }
                 nscan = hlen; extra = h2;
                 hlen += 1; h = h2; hx ^= h2; pass_count = 0;
@@ -569,7 +579,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, nscan, extra, lane);
+            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, lane);
         }
         __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit
