@@ -36,6 +36,7 @@ using namespace bbk;
 constexpr int kWarps = 4;             // warps (boards in flight) per CTA
 constexpr int kPlanes = 17;
 constexpr int kBloomBits = BBK_GO_BLOOM_WORDS * 32;   // 8192
+constexpr int kPatPrefetchOff = 2304;   // byte offset of the next board's pat inside the scratch union
 
 __host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
 
@@ -66,6 +67,10 @@ struct WarpSmem {
         } ob;
     } u;
     static_assert(MAXR * 4 >= BBK_GO_BLOOM_WORDS * 4, "parent array must hold the Bloom filter");
+    static_assert(N != 19 || (kPatPrefetchOff >= 4 * (C + 4) + 4 * ((C * 17 + 31) / 32 + 2) &&
+                              kPatPrefetchOff >= ((A + 47) & ~15) &&
+                              kPatPrefetchOff + 2 * pat_stride(N) <= (int)sizeof(u)),
+                  "pat prefetch must sit past the observation/mask scratch and inside the union");
     alignas(16) uint16_t pat[pat_stride(N)];
     uint32_t rX[32], rY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
     int32_t roff[33];
@@ -177,7 +182,7 @@ __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
     const uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
                              (uint32_t)(h >> 26) & (kBloomBits - 1)};
 #pragma unroll
-    for (int j = 0; j < 3; j++) gb[idx[j] >> 5] |= 1u << (idx[j] & 31);
+    for (int j = 0; j < 3; j++) atomicOr(&gb[idx[j] >> 5], 1u << (idx[j] & 31));   // RED: no round trip
 }
 
 __device__ __forceinline__ uint32_t up_row(uint32_t v, int lane) {
@@ -422,6 +427,24 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
     __syncwarp();
 }
 
+// One scalar column of board b per lane (lanes 0-9), loaded a board ahead so the
+// loads are in flight while the current board is processed; read back by shuffles.
+__device__ __forceinline__ uint64_t load_field(const StepParams& p, int64_t b, int lane) {
+    switch (lane) {
+        case 0: return p.in.terminated[b];
+        case 1: return p.in.truncated[b];
+        case 2: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
+        case 3: return p.in_s.role_to_move[b];
+        case 4: return p.in_s.pass_count[b];
+        case 5: return (uint32_t)p.in.step_count[b];
+        case 6: return p.in_s.hash[b];
+        case 7: return p.in_s.hist_xor[b];
+        case 8: return (uint32_t)p.in_s.hist_len[b];
+        case 9: return (uint64_t)p.actions[b];
+        default: return 0ull;
+    }
+}
+
 template <int N>
 __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
     if (threadIdx.x < 16) {
@@ -432,7 +455,7 @@ __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
+__global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
     constexpr int C = N * N;
     constexpr int A = C + 1;
     constexpr int PS = pat_stride(N);
@@ -445,29 +468,26 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
     const uint32_t rowm = lane < N ? ROW : 0u;
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     unsigned long long eps = 0;
+    // next-board prefetch: scalar columns in registers (lane j holds field j), `pat` via
+    // cp.async into an idle tail of the scratch union (not touched by mask/obs emission)
+    uint16_t* pat_pf = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(&S.u) + kPatPrefetchOff);
+    const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(p, b0, lane) : 0ull;
+    bool pat_ready = false;
 
-    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
-        if (!p.force_reset && b + nwarps < p.n) {
-            // Warm L2 with the NEXT board's inputs (14 lines of pat + Bloom, 10 scalar columns) so
-            // its loads hit L2 instead of HBM; costs no shared memory.
-            const int64_t nb = b + nwarps;
-            const char* ptr = nullptr;
-            if (lane < 6) ptr = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS) + 128 * lane;
-            else if (lane < 14) ptr = reinterpret_cast<const char*>(p.store.bloom + nb * (int64_t)BBK_GO_BLOOM_WORDS) +
-                                      128 * (lane - 6);
-            else if (lane == 14) ptr = reinterpret_cast<const char*>(p.in.terminated + nb);
-            else if (lane == 15) ptr = reinterpret_cast<const char*>(p.in.truncated + nb);
-            else if (lane == 16) ptr = reinterpret_cast<const char*>(p.in.step_count + nb);
-            else if (lane == 17) ptr = reinterpret_cast<const char*>(p.in.player_to_role + 2 * nb);
-            else if (lane == 18) ptr = reinterpret_cast<const char*>(p.in_s.role_to_move + nb);
-            else if (lane == 19) ptr = reinterpret_cast<const char*>(p.in_s.pass_count + nb);
-            else if (lane == 20) ptr = reinterpret_cast<const char*>(p.in_s.hash + nb);
-            else if (lane == 21) ptr = reinterpret_cast<const char*>(p.in_s.hist_xor + nb);
-            else if (lane == 22) ptr = reinterpret_cast<const char*>(p.in_s.hist_len + nb);
-            else if (lane == 23) ptr = reinterpret_cast<const char*>(p.actions + nb);
-            if (ptr) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+    for (int64_t b = b0; b < p.n; b += nwarps) {
+        if (!p.force_reset && b + nwarps < p.n && lane < 8) {
+            // warm L2 with the next board's Bloom filter (cp.async'd mid-board)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)BBK_GO_BLOOM_WORDS) + 128 * lane));
         }
-        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+        const uint64_t f_term = __shfl_sync(BBK_FULL, (uint32_t)pf, 0), f_trunc = __shfl_sync(BBK_FULL, (uint32_t)pf, 1);
+        const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)pf, 2), f_role = __shfl_sync(BBK_FULL, (uint32_t)pf, 3);
+        const uint32_t f_pass = __shfl_sync(BBK_FULL, (uint32_t)pf, 4), f_step = __shfl_sync(BBK_FULL, (uint32_t)pf, 5);
+        const uint64_t f_hash = shfl64(pf, 6), f_hx = shfl64(pf, 7);
+        const uint32_t f_hlen = __shfl_sync(BBK_FULL, (uint32_t)pf, 8);
+        const int64_t f_act = (int64_t)shfl64(pf, 9);
+        const bool reset = p.force_reset || f_term || f_trunc;
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
         uint32_t* gbloom = p.store.bloom + b * (int64_t)BBK_GO_BLOOM_WORDS;
@@ -491,12 +511,19 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             if (lane == 0) { bloom_add(gbloom, 0ull); hist[0] = 0ull; }
             nscan = 0; extra = 0ull;
         } else {
-            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
-            role = p.in_s.role_to_move[b]; pass_count = p.in_s.pass_count[b];
-            step = p.in.step_count[b];
-            h = p.in_s.hash[b]; hx = p.in_s.hist_xor[b]; hlen = p.in_s.hist_len[b];
-            const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
-            for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+            p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
+            role = (int)f_role; pass_count = (int)f_pass;
+            step = (int)f_step;
+            h = f_hash; hx = f_hx; hlen = (int)f_hlen;
+            if (pat_ready) {   // prefetched during the previous board
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+                for (int i = lane; i < PS / 8; i += 32)
+                    reinterpret_cast<uint4*>(S.pat)[i] = reinterpret_cast<const uint4*>(pat_pf)[i];
+            } else {
+                const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
+                for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+            }
             __syncwarp();
             if (lane < N) {
 #pragma unroll 4
@@ -506,7 +533,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
                     Wh |= ((v >> 1) & 1u) << col;
                 }
             }
-            const int a = (int)p.actions[b];
+            const int a = (int)f_act;
             step += 1;
             nscan = hlen; extra = h;
             if (a < 0 || a >= C) {   // pass (go.py:222-230)
@@ -622,6 +649,17 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(StepParams p) {
             if (lane == 0) p.out.next_actions[b] = act;
         }
         __syncwarp();   // staged mask bytes are overwritten by the observation pattern next
+        pat_ready = false;
+        if (!p.force_reset && b + nwarps < p.n) {   // issue the next board's loads now
+            const int64_t nb = b + nwarps;
+            pf = load_field(p, nb, lane);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
+            const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
+            for (int i = lane; i < PS / 8; i += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
+            asm volatile("cp.async.commit_group;");
+            pat_ready = true;
+        }
         if (p.out.observation) emit_obs<N>(S, B.lut, p.out.observation, b, role, lane);
         if (lane == 0) {
             float r0 = 0.0f, r1 = 0.0f;
