@@ -1,0 +1,63 @@
+"""Host-side API contract (no GPU): registry, specs, errors, key schedule (reference test_core.py:10-50)."""
+
+import pytest
+
+import paper_2303_17503_b200 as bb
+from paper_2303_17503_b200.games._device import Lineage
+
+EXPECTED = {
+    "go_9x9": (2, (9, 9, 17), 82),
+    "go_19x19": (2, (19, 19, 17), 362),
+    "backgammon": (2, (34,), 156),
+    "chess": (2, (8, 8, 119), 4672),
+    "shogi": (2, (9, 9, 119), 2187),
+}
+
+
+def test_registry_has_the_five_hot_path_games():
+    assert set(bb.available_games()) == set(EXPECTED)
+
+
+@pytest.mark.parametrize("game_id", sorted(EXPECTED))
+def test_specs_match_table(game_id):
+    spec = bb.game_spec(game_id)
+    assert (spec.num_players, spec.observation_shape, spec.num_actions) == EXPECTED[game_id]
+
+
+def test_reserved_and_unknown_ids():
+    for game_id in ("tic_tac_toe", "othello", "animal_shogi", "minatar_breakout"):
+        assert bb.game_spec(game_id).num_actions > 0
+        with pytest.raises(bb.UnsupportedGame):
+            bb.batch_init(game_id, bb.RngKey(0), 2)
+    with pytest.raises(bb.UnsupportedGame):
+        bb.game_spec("parcheesi")
+
+
+def test_empty_batch_rejected_before_any_device_work():
+    with pytest.raises(bb.EmptyBatch):
+        bb.batch_init("go_9x9", bb.RngKey(0), 0)
+
+
+def test_self_capture_variant_is_explicitly_unsupported():
+    from paper_2303_17503_b200.games import go
+
+    with pytest.raises(bb.UnsupportedGame):
+        go.make_game(9, allow_self_capture=True)
+    assert go.make_game(13).spec.num_actions == 170
+
+
+def test_lineage_allows_head_and_recent_branches():
+    lin = Lineage(1)
+    assert lin.depth(1) == 0
+    lin.advance(1, 2)
+    lin.advance(2, 3)
+    assert lin.depth(3) == 0 and lin.depth(2) == 1 and lin.depth(1) == 2 and lin.depth(99) > 2
+    lin.advance(2, 4)          # branch from the predecessor: 3 is dropped
+    assert lin.depth(4) == 0 and lin.depth(2) == 1 and lin.depth(3) > 2
+
+
+def test_session_key_schedule_matches_reference_formula():
+    # bench.py:54-83: init root.child(0), actions before step t root.child(2t-1), step t root.child(2t)
+    root = bb.RngKey(0)
+    assert root.child(0).state != root.child(1).state
+    assert bb.RngKey(0).state == 0xE220A8397B1DCDAF
