@@ -62,9 +62,13 @@ typedef struct bbk_cols {
  *   pat[n, pat_stride]  uint16: bit 2t / 2t+1 = black / white stone at the
  *                       point in boards_hist[t] (t = 0 newest .. 7)
  *   history[n, hist_cap] uint64 append-only superko hashes (history set)
- *   bloom[n, 256]        uint32 8192-bit Bloom filter over history
+ *   bloom[n, 320]        uint32: 8192-bit Bloom filter over history hashes, then a
+ *                        2048-bit filter of the (black, white) stone-count pairs of the
+ *                        history positions (a repeat must have equal counts)
  */
 #define BBK_GO_BLOOM_WORDS 256
+#define BBK_GO_PAIR_WORDS 64
+#define BBK_GO_FILTER_WORDS (BBK_GO_BLOOM_WORDS + BBK_GO_PAIR_WORDS)
 
 typedef struct bbk_go_state {
     uint16_t* pat;

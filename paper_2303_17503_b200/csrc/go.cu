@@ -45,7 +45,7 @@ struct WarpSmem {
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
     // >= max runs of both colours, and >= the Bloom filter's 256 words (it reuses `par`)
-    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32 > 256 ? ((N + 1) / 2) * 2 * N + 32 : 256;
+    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32 > BBK_GO_FILTER_WORDS ? ((N + 1) / 2) * 2 * N + 32 : BBK_GO_FILTER_WORDS;
     uint64_t capx[C];
     // Phase-multiplexed scratch (each member is dead before the next one is written):
     // group analysis -> superko hits -> staged mask bytes -> observation pattern.
@@ -57,7 +57,7 @@ struct WarpSmem {
             uint16_t root[MAXR];
         } uf;
         struct {
-            uint32_t bloom_area[BBK_GO_BLOOM_WORDS];
+            uint32_t bloom_area[BBK_GO_FILTER_WORDS];
             uint64_t hit[32];
         } sk;
         alignas(16) uint8_t mb[((A + 47) & ~15)];
@@ -66,7 +66,7 @@ struct WarpSmem {
             uint32_t W[(C * 17 + 31) / 32 + 2];
         } ob;
     } u;
-    static_assert(MAXR * 4 >= BBK_GO_BLOOM_WORDS * 4, "parent array must hold the Bloom filter");
+    static_assert(MAXR >= BBK_GO_FILTER_WORDS, "parent array must hold the Bloom + count-pair filter");
     static_assert(N != 19 || (kPatPrefetchOff >= 4 * (C + 4) + 4 * ((C * 17 + 31) / 32 + 2) &&
                               kPatPrefetchOff >= ((A + 47) & ~15) &&
                               kPatPrefetchOff + 2 * pat_stride(N) <= (int)sizeof(u)),
@@ -177,6 +177,16 @@ __device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
     return ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & (bloom[i3 >> 5] >> (i3 & 31)) & 1u) != 0;
 }
 
+// Stone-count pair filter: a position can only repeat a history position with the same
+// (black, white) stone counts; all non-capture candidates of a board share one pair.
+__device__ __forceinline__ uint32_t pair_idx(int nb, int nw) {
+    return ((uint32_t)((nb << 9) | nw) * 0x9E3779B1u) >> 21;   // 11 bits
+}
+__device__ __forceinline__ void pair_add(uint32_t* gb, int nb, int nw) {   // lane 0 only
+    const uint32_t i = pair_idx(nb, nw);
+    atomicOr(&gb[BBK_GO_BLOOM_WORDS + (i >> 5)], 1u << (i & 31));
+}
+
 // Lane 0 only: add h to the env's global filter.
 __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
     const uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
@@ -234,7 +244,8 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 // is balanced no matter how the stones are distributed over the rows.
 template <int N>
 __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y, uint32_t E, uint64_t h,
-                               const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra, int lane) {
+                               const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra,
+                               int nblack, int nwhite, int lane) {
     constexpr uint32_t ROW = (1u << N) - 1u;
     auto& U = S.u.uf;
     const int r = lane;
@@ -311,10 +322,10 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     const uint32_t* bl = U.par;
     {
         __threadfence_block();
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.par) + 16u * lane;
-        const char* src = reinterpret_cast<const char*>(gbloom) + 16 * lane;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 512u), "l"(src + 512));
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.par);
+        const char* src = reinterpret_cast<const char*>(gbloom);
+        for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
         asm volatile("cp.async.commit_group;");
     }
     // 3. atari classification; capture liberties (+ zobrist XOR) of opponent atari groups
@@ -351,8 +362,20 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     const uint32_t capb = lane < N ? S.rcap[lane] : 0u;
     const uint32_t NAu = up_row(NA, lane), NAd = dn_row(NA, lane);
     const uint32_t nb = ((E << 1) | (E >> 1) | Eu | Ed | (NA << 1) | (NA >> 1) | NAu | NAd) & ROW;
-    const uint32_t cand = E & (capb | nb);
+    uint32_t cand = E & (capb | nb);
     uint32_t legal = 0u, pend = 0u;
+    // one probe per board: if no history position had the stone counts a non-capture move
+    // produces, none of those moves can repeat a position -> no hash / Bloom work for them
+    bool pair_seen;
+    {
+        const int mb = ycol == 1 ? nblack + 1 : nblack, mw = ycol == 1 ? nwhite : nwhite + 1;   // mover = 1 - ycol
+        const uint32_t i = pair_idx(mb, mw);
+        pair_seen = (bl[BBK_GO_BLOOM_WORDS + (i >> 5)] >> (i & 31)) & 1u;
+    }
+    if (!pair_seen) {
+        legal = cand & ~capb;
+        cand &= capb;
+    }
     for (uint32_t c_ = cand; c_; c_ &= c_ - 1) {
         int p = __ffs(c_) - 1;
         int cell = r * N + p;
@@ -476,10 +499,10 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
     bool pat_ready = false;
 
     for (int64_t b = b0; b < p.n; b += nwarps) {
-        if (!p.force_reset && b + nwarps < p.n && lane < 8) {
+        if (!p.force_reset && b + nwarps < p.n && lane < 10) {
             // warm L2 with the next board's Bloom filter (cp.async'd mid-board)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)BBK_GO_BLOOM_WORDS) + 128 * lane));
+                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)BBK_GO_FILTER_WORDS) + 128 * lane));
         }
         const uint64_t f_term = __shfl_sync(BBK_FULL, (uint32_t)pf, 0), f_trunc = __shfl_sync(BBK_FULL, (uint32_t)pf, 1);
         const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)pf, 2), f_role = __shfl_sync(BBK_FULL, (uint32_t)pf, 3);
@@ -490,7 +513,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
         const bool reset = p.force_reset || f_term || f_trunc;
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
-        uint32_t* gbloom = p.store.bloom + b * (int64_t)BBK_GO_BLOOM_WORDS;
+        uint32_t* gbloom = p.store.bloom + b * (int64_t)BBK_GO_FILTER_WORDS;
         int8_t p2r0, p2r1;
         int role, pass_count, step, hlen;
         uint64_t h, hx;
@@ -505,10 +528,10 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
             role = 0; pass_count = 0; step = 0; h = 0ull; hx = 0ull; hlen = 1;
             for (int i = lane; i < PS; i += 32) S.pat[i] = 0;
-            for (int i = lane; i < BBK_GO_BLOOM_WORDS / 4; i += 32)
+            for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
                 reinterpret_cast<uint4*>(gbloom)[i] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
-            if (lane == 0) { bloom_add(gbloom, 0ull); hist[0] = 0ull; }
+            if (lane == 0) { bloom_add(gbloom, 0ull); pair_add(gbloom, 0, 0); hist[0] = 0ull; }
             nscan = 0; extra = 0ull;
         } else {
             p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
@@ -577,9 +600,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
                 O &= ~dead;
                 const uint64_t h2 = h ^ zkey<N>(a, role) ^ warp_xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
+                const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
                 if (lane == 0) {
                     hist[hlen] = h2;
                     bloom_add(gbloom, h2);
+                    pair_add(gbloom, nbk, nwh);
                 }
                 nscan = hlen; extra = h2;
                 hlen += 1; h = h2; hx ^= h2; pass_count = 0;
@@ -606,7 +631,8 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, lane);
+            const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
+            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, lane);
         }
         __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit
@@ -724,7 +750,10 @@ __global__ void rebuild_bloom_kernel(bbk_go_store st, const int32_t* hist_len, i
             atomicOr(&sb[w][i3 >> 5], 1u << (i3 & 31));
         }
         __syncwarp();
-        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) st.bloom[b * BBK_GO_BLOOM_WORDS + i] = sb[w][i];
+        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) st.bloom[b * BBK_GO_FILTER_WORDS + i] = sb[w][i];
+        // history keeps no stone counts: mark every pair as seen (correct, only slower)
+        for (int i = lane; i < BBK_GO_PAIR_WORDS; i += 32)
+            st.bloom[b * BBK_GO_FILTER_WORDS + BBK_GO_BLOOM_WORDS + i] = 0xFFFFFFFFu;
         __syncwarp();
     }
 }

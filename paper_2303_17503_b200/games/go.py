@@ -102,7 +102,7 @@ class GoKernel(DeviceKernel):
         torch = _torch()
         cap = int(limit) + 2
         hist = torch.empty((n, cap), dtype=torch.int64, device=device)
-        bloom = torch.empty((n, 256), dtype=torch.int32, device=device)
+        bloom = torch.empty((n, 320), dtype=torch.int32, device=device)   # BBK_GO_FILTER_WORDS
         return GoStore(hist, bloom, cap)
 
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
