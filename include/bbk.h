@@ -61,6 +61,8 @@ typedef struct bbk_cols {
  * observe :264-273, Core.encode :103-111.
  *   pat[n, pat_stride]  uint16: bit 2t / 2t+1 = black / white stone at the
  *                       point in boards_hist[t] (t = 0 newest .. 7)
+ *   lab[n, pat_stride]  uint16: chain label per stone = one point of the stone's chain
+ *                       (maintained incrementally; values at empty points are don't-care)
  *   history[n, hist_cap] uint64 append-only superko hashes (history set)
  *   bloom[n, 320]        uint32: 8192-bit Bloom filter over history hashes, then a
  *                        2048-bit filter of the (black, white) stone-count pairs of the
@@ -72,6 +74,7 @@ typedef struct bbk_cols {
 
 typedef struct bbk_go_state {
     uint16_t* pat;
+    uint16_t* lab;      /* [n, pat_stride] chain label of every stone (a point of its chain) */
     uint64_t* hash;
     uint64_t* hist_xor;
     int32_t*  hist_len;

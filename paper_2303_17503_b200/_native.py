@@ -38,7 +38,7 @@ class Cols(C.Structure):
 
 
 class GoState(C.Structure):
-    _fields_ = [("pat", P), ("hash", P), ("hist_xor", P), ("hist_len", P), ("role_to_move", P),
+    _fields_ = [("pat", P), ("lab", P), ("hash", P), ("hist_xor", P), ("hist_len", P), ("role_to_move", P),
                 ("pass_count", P)]
 
 

@@ -10,11 +10,11 @@
 // (black, white, empty; bit c = column c). Per step:
 //   1. placement + captures: bit-parallel flood of each enemy neighbour
 //      group over the rows (shuffles), captured iff no liberty;
-//   2. analysis of the new board: union-find over horizontal RUNS (not
-//      cells) in shared memory, hooked with atomicCAS between vertically
-//      overlapping runs; per group "is in atari" from one atomicOr per run of
-//      OR(lib) | OR(~lib) (a group has exactly one liberty iff every
-//      liberty position is equal iff the two ORs are disjoint);
+//   2. analysis of the new board: chains carry a persistent label (one point
+//      of the chain, `lab`), updated incrementally at placement (a merge
+//      relabels the absorbed chains); per chain "is in atari" from one
+//      atomicOr per horizontal run of OR(lib) | OR(~lib) (a chain has exactly
+//      one liberty iff every liberty position is equal iff the ORs are disjoint);
 //   3. legal mask: empty points with an empty neighbour / a non-atari own
 //      neighbour group / a capture (XOR of the captured atari groups'
 //      zobrist accumulated at their single liberty), filtered by positional
@@ -36,25 +36,32 @@ using namespace bbk;
 constexpr int kWarps = 4;             // warps (boards in flight) per CTA
 constexpr int kPlanes = 17;
 constexpr int kBloomBits = BBK_GO_BLOOM_WORDS * 32;   // 8192
-constexpr int kPatPrefetchOff = 2304;   // byte offset of the next board's pat inside the scratch union
 
 __host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
+
+// byte offset of the next board's prefetched pat (then lab) inside the scratch union:
+// past the observation and mask scratch, which are live while the prefetch is in flight
+__host__ __device__ constexpr int pf_off(int N) {
+    const int ob = 4 * (N * N + 4) + 4 * ((N * N * 17 + 31) / 32 + 2), mb = (N * N + 1 + 47) & ~15;
+    return ((ob > mb ? ob : mb) + 15) & ~15;
+}
 
 template <int N>
 struct WarpSmem {
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
-    // >= max runs of both colours, and >= the Bloom filter's 256 words (it reuses `par`)
-    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32 > BBK_GO_FILTER_WORDS ? ((N + 1) / 2) * 2 * N + 32 : BBK_GO_FILTER_WORDS;
+    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
     uint64_t capx[C];
     // Phase-multiplexed scratch (each member is dead before the next one is written):
-    // group analysis -> superko hits -> staged mask bytes -> observation pattern.
+    // chain labels -> group analysis -> superko hits -> staged mask bytes -> observation pattern.
     union {
         struct {
-            uint32_t par[MAXR];    // union-find over run indices; then the env's Bloom filter (cp.async)
+            // the board's chain labels (u16) until the run list is built; then the env's
+            // Bloom + count-pair filter (cp.async)
+            alignas(16) uint32_t bl[BBK_GO_FILTER_WORDS];
             uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
-            uint32_t gst[MAXR];    // OR(lib) | OR(~lib) << 10 | HAS, at group roots
-            uint16_t root[MAXR];
+            uint16_t root[MAXR];   // chain label of the run
+            uint32_t gst[C];       // OR(lib) | OR(~lib) << 10 | HAS, by chain label
         } uf;
         struct {
             uint32_t bloom_area[BBK_GO_FILTER_WORDS];
@@ -66,49 +73,16 @@ struct WarpSmem {
             uint32_t W[(C * 17 + 31) / 32 + 2];
         } ob;
     } u;
-    static_assert(MAXR >= BBK_GO_FILTER_WORDS, "parent array must hold the Bloom + count-pair filter");
-    static_assert(N != 19 || (kPatPrefetchOff >= 4 * (C + 4) + 4 * ((C * 17 + 31) / 32 + 2) &&
-                              kPatPrefetchOff >= ((A + 47) & ~15) &&
-                              kPatPrefetchOff + 2 * pat_stride(N) <= (int)sizeof(u)),
-                  "pat prefetch must sit past the observation/mask scratch and inside the union");
+    static_assert(2 * pat_stride(N) <= 4 * BBK_GO_FILTER_WORDS, "labels must fit the filter landing area");
+    static_assert(pf_off(N) + 4 * pat_stride(N) <= (int)sizeof(u), "pat + lab prefetch must fit the union");
     alignas(16) uint16_t pat[pat_stride(N)];
     uint32_t rX[32], rY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
     int32_t roff[33];
 };
 
-// Zobrist tables (go.py:20-25): zob[2*cell + colour] = mix64(base + 2*cell + colour),
-// base = 0x60D00D60C0FFEE00 + N. Evaluated at compile time into read-only global
-// memory (L1-cached via __ldg) so they cost no shared memory.
-struct ZobTables {
-    uint64_t v[3][2 * 19 * 19];
-};
-__host__ __device__ constexpr uint64_t cmix64(uint64_t x) {
-    x ^= x >> 30;
-    x *= 0xBF58476D1CE4E5B9ULL;
-    x ^= x >> 27;
-    x *= 0x94D049BB133111EBULL;
-    return x ^ (x >> 31);
-}
-constexpr ZobTables make_zob() {
-    ZobTables z{};
-    const int sizes[3] = {9, 13, 19};
-    for (int k = 0; k < 3; k++) {
-        const int n = sizes[k];
-        const uint64_t base = 0x60D00D60C0FFEE00ULL + (uint64_t)n;
-        for (int i = 0; i < 2 * n * n; i++) {
-            const int cell = i % (n * n), colour = i / (n * n);   // [0,C) black, [C,2C) white
-            z.v[k][i] = cmix64(base + 2ull * (uint64_t)cell + (uint64_t)colour);
-        }
-    }
-    return z;
-}
-__device__ const ZobTables g_zob = make_zob();
-template <int N>
-__device__ __forceinline__ const uint64_t* zob_table() {
-    return g_zob.v[N == 9 ? 0 : N == 13 ? 1 : 2];
-}
-// zobrist key of (cell, colour) computed in registers: with shared memory taking
-// most of the unified L1, a table lookup would be an L2 round trip; mix64 is ~15 ALU ops.
+// zobrist key of (cell, colour) (go.py:20-25): mix64(0x60D00D60C0FFEE00 + N + 2*cell + colour),
+// computed in registers: with shared memory taking most of the unified L1, a table lookup
+// would be an L2 round trip; mix64 is ~15 ALU ops.
 template <int N>
 __device__ __forceinline__ uint64_t zkey(int cell, int colour) {
     return mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)cell + (uint64_t)colour);
@@ -138,36 +112,6 @@ struct StepParams {
 __device__ __forceinline__ uint32_t run_at(uint32_t X, int s) {
     uint32_t len = __ffs(~(X >> s)) - 1;
     return ((1u << len) - 1u) << s;
-}
-
-__device__ __forceinline__ uint32_t uf_find(volatile uint32_t* par, uint32_t x) {
-    uint32_t p;
-    while ((p = par[x]) != x) x = p;
-    return x;
-}
-
-// find with path halving; racing lanes only ever re-point a node at one of its
-// ancestors, so the forest stays valid while other lanes hook roots with CAS.
-__device__ __forceinline__ uint32_t uf_find_halve(volatile uint32_t* par, uint32_t x) {
-    while (true) {
-        const uint32_t p = par[x];
-        if (p == x) return x;
-        const uint32_t gp = par[p];
-        if (gp != p) par[x] = gp;
-        x = gp;
-    }
-}
-
-__device__ __forceinline__ void uf_union(uint32_t* par, uint32_t a, uint32_t b) {
-    volatile uint32_t* vp = par;
-    while (true) {
-        a = uf_find_halve(vp, a);
-        b = uf_find_halve(vp, b);
-        if (a == b) return;
-        if (a < b) { uint32_t t = a; a = b; b = t; }
-        const uint32_t old = atomicCAS(&par[a], a, b);
-        if (old == a) return;
-    }
 }
 
 __device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
@@ -262,50 +206,30 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     S.rX[lane] = X; S.rY[lane] = Y; S.rE[lane] = E; S.rcap[lane] = 0u;
     S.roff[lane] = off;
     if (lane == 31) S.roff[32] = total;
-    {   // this row's runs -> list
+    {   // this row's runs -> list, each with its chain label
+        const uint16_t* lab = reinterpret_cast<const uint16_t*>(U.bl);
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
             U.run[k] = (uint16_t)((0u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(X >> s)) - 1));
+            const uint16_t l = lab[r * N + s];
+            U.root[k] = l;
+            U.gst[l] = 0u;
         }
         for (uint32_t s_ = SY; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
             U.run[k] = (uint16_t)((1u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(Y >> s)) - 1));
+            const uint16_t l = lab[r * N + s];
+            U.root[k] = l;
+            U.gst[l] = 0u;
         }
     }
-    for (int i = lane; i < total; i += 32) { U.par[i] = (uint32_t)i; U.gst[i] = 0u; }
     for (int i = lane; i < (N * N + 1) / 2; i += 32)
         reinterpret_cast<uint4*>(S.capx)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
-    // 1. hook each run to the overlapping same-colour runs of the row above
+    // liberty OR-stats per chain
     for (int i = lane; i < total; i += 32) {
-        const uint32_t e = U.run[i];
-        const int rr = (e >> 10) & 31;
-        if (rr == 0) continue;
-        const int col = e >> 15, s = (e >> 5) & 31, len = e & 31;
-        const uint32_t Zu = col ? S.rY[rr - 1] : S.rX[rr - 1];
-        const uint32_t Su = Zu & ~(Zu << 1);   // run starts of the row above
-        const int base = S.roff[rr - 1] + (col ? __popc(S.rX[rr - 1] & ~(S.rX[rr - 1] << 1)) : 0);
-        uint32_t V = (((1u << len) - 1u) << s) & Zu;
-        while (V) {
-            const int c = __ffs(V) - 1;
-            const int st = 31 - __clz(Su & ((2u << c) - 1u));
-            V &= ~run_at(Zu, st);
-            uf_union(U.par, (uint32_t)i, (uint32_t)(base + __popc(Su & ((1u << st) - 1u))));
-        }
-    }
-    __syncwarp();
-    // 2. flatten (path halving; chains are static now) + liberty OR-stats per group root
-    for (int i = lane; i < total; i += 32) {
-        uint32_t x = (uint32_t)i;
-        while (true) {   // every write points at an ancestor, so racing lanes stay consistent
-            const uint32_t p = U.par[x];
-            if (p == x) break;
-            const uint32_t gp = U.par[p];
-            U.par[x] = gp;
-            x = gp;
-        }
-        U.root[i] = (uint16_t)x;
+        const uint32_t x = U.root[i];
         const uint32_t e = U.run[i];
         const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
         const uint32_t run = ((1u << len) - 1u) << s;
@@ -317,12 +241,12 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         atomicOr(&U.gst[x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
     __syncwarp();
-    // the parent array is dead now: async-copy this env's 1 KB Bloom filter into it, overlapped
+    // the labels are dead now: async-copy this env's Bloom + pair filter over them, overlapped
     // with the classification pass (it includes the hash appended by this step)
-    const uint32_t* bl = U.par;
+    const uint32_t* bl = U.bl;
     {
         __threadfence_block();
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.par);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.bl);
         const char* src = reinterpret_cast<const char*>(gbloom);
         for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
@@ -493,7 +417,9 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
     unsigned long long eps = 0;
     // next-board prefetch: scalar columns in registers (lane j holds field j), `pat` via
     // cp.async into an idle tail of the scratch union (not touched by mask/obs emission)
-    uint16_t* pat_pf = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(&S.u) + kPatPrefetchOff);
+    uint16_t* pat_pf = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(&S.u) + pf_off(N));
+    uint16_t* lab_pf = pat_pf + PS;
+    uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
     const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(p, b0, lane) : 0ull;
     bool pat_ready = false;
@@ -527,7 +453,9 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             int c = (int)(child(k, 0) % 2ull);
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
             role = 0; pass_count = 0; step = 0; h = 0ull; hx = 0ull; hlen = 1;
-            for (int i = lane; i < PS; i += 32) S.pat[i] = 0;
+            // the discarded prefetch of this board must land before the scratch is reused
+            if (pat_ready) asm volatile("cp.async.wait_all;" ::: "memory");
+            for (int i = lane; i < PS; i += 32) { S.pat[i] = 0; lab[i] = 0; }
             for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
                 reinterpret_cast<uint4*>(gbloom)[i] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
@@ -541,11 +469,17 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             if (pat_ready) {   // prefetched during the previous board
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
-                for (int i = lane; i < PS / 8; i += 32)
+                for (int i = lane; i < PS / 8; i += 32) {
                     reinterpret_cast<uint4*>(S.pat)[i] = reinterpret_cast<const uint4*>(pat_pf)[i];
+                    reinterpret_cast<uint4*>(lab)[i] = reinterpret_cast<const uint4*>(lab_pf)[i];
+                }
             } else {
                 const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
-                for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+                const uint4* lsrc = reinterpret_cast<const uint4*>(p.in_s.lab + b * (int64_t)PS);
+                for (int i = lane; i < PS / 8; i += 32) {
+                    reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+                    reinterpret_cast<uint4*>(lab)[i] = lsrc[i];
+                }
             }
             __syncwarp();
             if (lane < N) {
@@ -568,6 +502,27 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             } else {                 // placement (go.py:232-262)
                 const int ra = a / N, ca = a - ra * N;
                 uint32_t M = role == 0 ? Bk : Wh, O = role == 0 ? Wh : Bk;
+                {   // chain label of the new stone: the first own neighbour's, absorbing the others
+                    const uint32_t Mr = __shfl_sync(BBK_FULL, M, ra);
+                    const uint32_t Mu = __shfl_sync(BBK_FULL, M, ra > 0 ? ra - 1 : 0);
+                    const uint32_t Md = __shfl_sync(BBK_FULL, M, ra < N - 1 ? ra + 1 : 0);
+                    constexpr uint32_t NONE = 0xFFFFu;   // never a label (labels < C)
+                    const uint32_t lu = (ra > 0 && ((Mu >> ca) & 1u)) ? lab[a - N] : NONE;
+                    const uint32_t ld = (ra < N - 1 && ((Md >> ca) & 1u)) ? lab[a + N] : NONE;
+                    const uint32_t ll = (ca > 0 && ((Mr >> (ca - 1)) & 1u)) ? lab[a - 1] : NONE;
+                    const uint32_t lr = (ca < N - 1 && ((Mr >> (ca + 1)) & 1u)) ? lab[a + 1] : NONE;
+                    const uint32_t L0 = lu != NONE ? lu : ld != NONE ? ld : ll != NONE ? ll : lr != NONE ? lr : (uint32_t)a;
+                    __syncwarp();
+                    if ((ld != NONE && ld != L0) | (ll != NONE && ll != L0) | (lr != NONE && lr != L0)) {
+                        for (uint32_t m_ = M; m_; m_ &= m_ - 1) {   // lanes >= N hold no stones
+                            const int cell = lane * N + __ffs(m_) - 1;
+                            const uint32_t l = lab[cell];
+                            if (l == ld || l == ll || l == lr) lab[cell] = (uint16_t)L0;
+                        }
+                    }
+                    if (lane == 0) lab[a] = (uint16_t)L0;
+                    __syncwarp();
+                }
                 if (lane == ra) M |= 1u << ca;
                 const uint32_t E0 = ~(M | O) & rowm;
                 uint64_t capxor = 0ull;
@@ -623,8 +578,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             }
         }
         __syncwarp();
-        for (int i = lane; i < PS / 8; i += 32)
+        uint16_t* olab = p.out_s.lab + b * (int64_t)PS;
+        for (int i = lane; i < PS / 8; i += 32) {
             reinterpret_cast<uint4*>(opat)[i] = reinterpret_cast<const uint4*>(S.pat)[i];
+            reinterpret_cast<uint4*>(olab)[i] = reinterpret_cast<const uint4*>(lab)[i];
+        }
         const bool truncated = !terminal && step >= p.max_steps;
         // legal mask of the new mover (skipped once the slot is finished)
         uint32_t legal = 0u;
@@ -681,8 +639,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             pf = load_field(p, nb, lane);
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
             const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
-            for (int i = lane; i < PS / 8; i += 32)
+            const char* lsrc = reinterpret_cast<const char*>(p.in_s.lab + nb * (int64_t)PS);
+            for (int i = lane; i < PS / 8; i += 32) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 2u * PS + 16u * i), "l"(lsrc + 16 * i));
+            }
             asm volatile("cp.async.commit_group;");
             pat_ready = true;
         }

@@ -8,6 +8,7 @@ actions, max_steps 512; go.py:282-290) whose ``batch_kernel`` runs
 Device state per slot (besides the public columns):
   pat[PS] int16   transposed 8-deep board history (bit 2t/2t+1: black/white
                   stone in boards_hist[t]); replaces ``board`` + ``boards_hist``
+  lab[PS] int16   chain label per stone (a point of its chain), kept incrementally
   hash, hist_xor int64 (u64), hist_len int32, role_to_move, pass_count u8
 and a per-lineage append-only superko store: history[hist_cap] u64 and an
 8192-bit Bloom filter. The store is shared along a trajectory; a batch up
@@ -87,6 +88,7 @@ class GoKernel(DeviceKernel):
         n, dev = v.n, v.device
         p = v.priv
         p.pat = torch.empty((n, self.pat_stride), dtype=torch.int16, device=dev)
+        p.lab = torch.empty((n, self.pat_stride), dtype=torch.int16, device=dev)
         p.hash = torch.empty(n, dtype=torch.int64, device=dev)
         p.hist_xor = torch.empty(n, dtype=torch.int64, device=dev)
         p.hist_len = torch.empty(n, dtype=torch.int32, device=dev)
@@ -95,7 +97,7 @@ class GoKernel(DeviceKernel):
 
     def state_struct(self, v: DeviceV) -> nat.GoState:
         p = v.priv
-        return nat.GoState(nat.ptr(p.pat), nat.ptr(p.hash), nat.ptr(p.hist_xor), nat.ptr(p.hist_len),
+        return nat.GoState(nat.ptr(p.pat), nat.ptr(p.lab), nat.ptr(p.hash), nat.ptr(p.hist_xor), nat.ptr(p.hist_len),
                            nat.ptr(p.role_to_move), nat.ptr(p.pass_count))
 
     def new_store(self, n: int, limit: int, device) -> GoStore:
