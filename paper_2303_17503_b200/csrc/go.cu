@@ -354,6 +354,17 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
     }
     if (lane < 4) P[C + lane] = 0u;
     __syncwarp();
+    // the record as a bit stream: bit f of W = float f (17 bits per point)
+    uint32_t* W = S.u.ob.W;
+    constexpr int NW = (NF + 31) / 32;
+    for (int w = lane; w < NW; w += 32) {
+        const uint32_t q = 32u * w, c = (q * 61681u) >> 20, k = q - 17u * c;   // q / 17, exact for q < 65536
+        uint32_t v = (P[c] >> k) | (P[c + 1] << (17 - k));
+        if (k > 2) v |= P[c + 2] << (34 - k);
+        W[w] = v;
+    }
+    if (lane == 0) W[NW] = 0u;
+    __syncwarp();
     const int64_t F0 = b * (int64_t)NF;
     const int head = (int)((4 - (F0 & 3)) & 3);             // floats before the first aligned chunk
     const int nchunk = (NF - head) >> 2;
@@ -361,16 +372,16 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
     const int tail0 = head + 4 * nchunk;
     if (lane < head || (lane >= 4 && lane - 4 < NF - tail0)) {
         const uint32_t fi = lane < 4 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 4);
-        const uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;
-        rec[fi] = (float)((P[c] >> k) & 1u);
+        rec[fi] = (float)((W[fi >> 5] >> (fi & 31)) & 1u);
     }
+    // chunk j = lane + 32 m starts at bit head + 4 lane + 128 m: a lane-constant bit
+    // offset in word (head + 4 lane) / 32 + 4 m
     float4* o4 = reinterpret_cast<float4*>(rec + head);
-    for (int j = lane; j < nchunk; j += 32) {
-        const uint32_t fi = (uint32_t)(head + 4 * j);
-        const uint32_t c = (fi * 61681u) >> 20, k = fi - 17u * c;   // fi / 17, exact for fi < 65536
-        const uint64_t w = (uint64_t)P[c] | ((uint64_t)P[c + 1] << 17);
-        o4[j] = lut[(uint32_t)(w >> k) & 15u];
-    }
+    const uint32_t q0 = (uint32_t)(head + 4 * lane), sh = q0 & 31u;
+    const uint32_t* wp = W + (q0 >> 5);
+#pragma unroll 4
+    for (int j = lane; j < nchunk; j += 32, wp += 4)
+        o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
     __syncwarp();
 }
 
