@@ -46,6 +46,10 @@ struct WarpSmem {
     uint64_t pinray[8];
     int8_t pinsq[8];
     uint16_t task[2][136];             // (piece, ray) work units: own [0], opponent [1]
+    // next-board prefetch (cp.async): board, packed past boards t = 1..7, ring meta by ply
+    alignas(16) uint8_t pf_bd[64];
+    alignas(16) uint8_t pf_past[7][32];
+    alignas(16) uint32_t pf_meta[RING];
 };
 
 struct Params {
@@ -312,12 +316,53 @@ __device__ void apply_action(uint8_t* bd, int& stm, int& castle, int& ep, int& h
     stm ^= 1;
 }
 
-__device__ __forceinline__ void load_past(uint8_t* dst, const uint8_t* hist_env, int ply, int lane) {
-    // packed nibble board of ply -> 64 piece bytes (absolute squares)
-    const uint8_t* src = hist_env + (ply & (RING - 1)) * 32;
-    uint8_t byte = src[lane];
-    dst[2 * lane] = byte & 15;
-    dst[2 * lane + 1] = byte >> 4;
+// One scalar field of board b per lane (lanes 0-4), loaded a board ahead.
+__device__ __forceinline__ uint64_t load_field(const Params& p, int64_t b, int lane) {
+    switch (lane) {
+        case 0: return (uint32_t)p.in.terminated[b] | ((uint32_t)p.in.truncated[b] << 8);
+        case 1: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
+        case 2: return *reinterpret_cast<const uint64_t*>(p.in_s.misc + b * 8);
+        case 3: return (uint32_t)p.in.step_count[b];
+        case 4: return (uint64_t)p.actions[b];
+        default: return 0ull;
+    }
+}
+
+// cp.async board b's state and the ring entries its step reads into the prefetch
+// area: the board, the packed boards of plies step-1..step-7 (step = in step + 1)
+// and the ring meta of plies [step - M, step) with M covering both the
+// observation history and the repetition window (half-move clock + 1 bound).
+__device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int64_t b, uint64_t f, int lane) {
+    const uint32_t term = (uint32_t)__shfl_sync(BBK_FULL, (uint32_t)f, 0);
+    const uint64_t misc = shfl64(f, 2);
+    const int in_step = (int)__shfl_sync(BBK_FULL, (uint32_t)f, 3);
+    const char* bsrc = reinterpret_cast<const char*>(p.in_s.board + b * 64);
+    if (lane < 4) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(S.pf_bd) + 16u * lane;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(bsrc + 16 * lane));
+    }
+    if (!(term & 0xFFFFu)) {
+        const uint8_t* hist = p.out_s.hist + b * (int64_t)HIST_BYTES;
+        const int step = in_step + 1;
+        if (lane < 14) {   // past boards t = 1 + lane / 2
+            const int ply = step - 1 - (lane >> 1);
+            if (ply >= 0) {
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&S.pf_past[lane >> 1][0]) + 16u * (lane & 1);
+                const char* src = reinterpret_cast<const char*>(hist + (ply & (RING - 1)) * 32) + 16 * (lane & 1);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+            }
+        }
+        const int hm1 = (int)((misc >> 24) & 0xFF) + 1;
+        int M = hm1 > 7 ? hm1 : 7;
+        if (M > step) M = step;
+        const uint32_t* meta = reinterpret_cast<const uint32_t*>(hist + RING * 32);
+        for (int j = lane; j < M; j += 32) {
+            const int ply = (step - 1 - j) & (RING - 1);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&S.pf_meta[ply]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(meta + ply));
+        }
+    }
+    asm volatile("cp.async.commit_group;");
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
@@ -332,8 +377,21 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
     const int lane = lane_id();
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     unsigned long long eps = 0;
-    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
-        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+    const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    uint64_t cur = 0ull;   // this board's scalar fields (lane j holds field j)
+    bool pf_ready = false;
+    for (int64_t b = b0; b < p.n; b += nwarps) {
+        if (!p.force_reset && !pf_ready) {   // first board of the warp: fetch synchronously
+            cur = load_field(p, b, lane);
+            issue_prefetch(S, p, b, cur, lane);
+        }
+        // the next board's scalars are in flight while this board is processed
+        const int64_t nb = b + nwarps;
+        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(p, nb, lane) : 0ull;
+        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0);
+        const bool reset = p.force_reset || (f_term & 0xFFFFu) != 0u;
+        if (!p.force_reset) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint8_t* hist = p.out_s.hist + b * (int64_t)HIST_BYTES;
         uint32_t* hmeta = reinterpret_cast<uint32_t*>(hist + RING * 32);
@@ -350,14 +408,29 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             }
             stm = 0; castle = 15; ep = -1; halfmove = 0; step = 0;
         } else {
-            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
-            const uint8_t* ib = p.in_s.board + b * 64;
-            S.bd[lane] = ib[lane]; S.bd[lane + 32] = ib[lane + 32];
-            const uint8_t* m = p.in_s.misc + b * 8;
-            stm = m[0]; castle = m[1]; ep = (int8_t)m[2]; halfmove = m[3];
-            step = p.in.step_count[b] + 1;
+            const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)cur, 1);
+            const uint64_t misc = shfl64(cur, 2);
+            const int f_step = (int)__shfl_sync(BBK_FULL, (uint32_t)cur, 3);
+            const int f_act = (int)shfl64(cur, 4);
+            p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
+            S.bd[lane] = S.pf_bd[lane]; S.bd[lane + 32] = S.pf_bd[lane + 32];
+            stm = (int)(misc & 0xFF); castle = (int)((misc >> 8) & 0xFF); ep = (int8_t)((misc >> 16) & 0xFF);
+            halfmove = (int)((misc >> 24) & 0xFF);
+            step = f_step + 1;
+            // past boards t = 1..7 from the prefetched packed copies
+            for (int t = 1; t < 8; t++) {
+                if (step - t >= 0) {
+                    const uint8_t byte = S.pf_past[t - 1][lane];
+                    S.past[t][2 * lane] = byte & 15;
+                    S.past[t][2 * lane + 1] = byte >> 4;
+                    if (lane == 0) S.prep[t] = (uint8_t)(S.pf_meta[(step - t) & (RING - 1)] >> 24);
+                } else {
+                    S.past[t][lane] = 0; S.past[t][lane + 32] = 0;
+                    if (lane == 0) S.prep[t] = 0;
+                }
+            }
             __syncwarp();
-            if (lane == 0) apply_action(S.bd, stm, castle, ep, halfmove, (int)p.actions[b]);
+            if (lane == 0) apply_action(S.bd, stm, castle, ep, halfmove, f_act);
             stm = __shfl_sync(BBK_FULL, stm, 0); castle = __shfl_sync(BBK_FULL, castle, 0);
             ep = __shfl_sync(BBK_FULL, ep, 0); halfmove = __shfl_sync(BBK_FULL, halfmove, 0);
         }
@@ -449,7 +522,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         const int window = halfmove < step ? halfmove : step;
         for (int j = lane; 2 * (j + 1) <= window; j += 32) {
             const int ply = step - 2 * (j + 1);
-            const uint32_t m = hmeta[ply & (RING - 1)];
+            const uint32_t m = S.pf_meta[ply & (RING - 1)];   // window <= half-move clock: prefetched
             if ((m & 0xFFFFFFu) == meta_key) {
                 const uint4* hb = reinterpret_cast<const uint4*>(hist + (ply & (RING - 1)) * 32);
                 const uint4* cb = reinterpret_cast<const uint4*>(S.packed);
@@ -497,16 +570,18 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             reinterpret_cast<const uint4*>(S.packed)[lane];
         if (lane == 0) hmeta[step & (RING - 1)] = meta_key | ((uint32_t)rep << 24);
         S.past[0][lane] = S.bd[lane]; S.past[0][lane + 32] = S.bd[lane + 32];
-        for (int t = 1; t < 8; t++) {
-            if (step - t >= 0) {
-                load_past(S.past[t], hist, step - t, lane);
-                if (lane == 0) S.prep[t] = (uint8_t)(hmeta[(step - t) & (RING - 1)] >> 24);
-            } else {
-                S.past[t][lane] = 0; S.past[t][lane + 32] = 0;
-                if (lane == 0) S.prep[t] = 0;
-            }
+        if (reset) {
+            for (int t = 1; t < 8; t++) { S.past[t][lane] = 0; S.past[t][lane + 32] = 0; }
+            if (lane < 8) S.prep[lane] = 0;
         }
         if (lane == 0) S.prep[0] = (uint8_t)rep;
+        __syncwarp();   // the prefetch area is free now: issue the next board's state
+        pf_ready = false;
+        if (!p.force_reset && nb < p.n) {
+            issue_prefetch(S, p, nb, nxt, lane);
+            cur = nxt;
+            pf_ready = true;
+        }
         for (int i = lane; i < NF / 32 + 4; i += 32) S.bits[i] = 0u;
         __syncwarp();
         // ---- observation bitstream: square v (mover frame) owns bits [119 v, 119 v + 119)

@@ -81,28 +81,42 @@ namespace bbk {
 // agents.random_actions (reference agents.py:33-46) for ONE slot whose legal
 // mask is staged in shared memory as 0/1 bytes at mask[0..A): returns the
 // index of the d-th legal action, d = child(key, slot) % max(count, 1), or 0.
-// Warp-cooperative: lanes count contiguous word ranges, scan, and the lane
-// holding the d-th set byte resolves it. `mask` may be unaligned.
+// Warp-cooperative: lanes count contiguous ranges of 16-byte chunks (bytes
+// outside [0, A) masked off), scan, and the lane holding the d-th set byte
+// resolves it. `mask` may be unaligned (chunks are taken from the 16-byte
+// aligned address at or below it).
+__device__ __forceinline__ uint32_t chunk_count_bytes(uint4 v) {
+    return __popc(v.x & 0x01010101u) + __popc(v.y & 0x01010101u) + __popc(v.z & 0x01010101u) +
+           __popc(v.w & 0x01010101u);
+}
 __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A, int count, uint64_t key,
                                                      int64_t slot) {
     if (count <= 0) return 0;
     const int lane = lane_id();
     const int d = (int)(child(key, (uint64_t)slot) % (uint64_t)count);
     const uintptr_t base = reinterpret_cast<uintptr_t>(mask);
-    const int head = (int)(base & 3);
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(base - head);
-    const int nw = (head + A + 3) >> 2;
-    const int per = (nw + 31) >> 5;
-    const int w0 = lane * per, w1 = min(w0 + per, nw);
-    auto word_at = [&](int i) -> uint32_t {
-        uint32_t v = w[i] & 0x01010101u;
-        const int b0 = 4 * i - head;                     // row byte of the word's byte 0
-        if (b0 < 0) v &= 0xFFFFFFFFu << (8 * (-b0));
-        if (b0 + 4 > A) v &= 0xFFFFFFFFu >> (8 * (b0 + 4 - A));
+    const int head = (int)(base & 15);
+    const uint4* w = reinterpret_cast<const uint4*>(base - head);
+    const int nc = (head + A + 15) >> 4;
+    const int per = (nc + 31) >> 5;
+    const int c0 = lane * per, c1 = min(c0 + per, nc);
+    // chunk i covers record bytes [16 i - head, 16 i - head + 16); clear the bytes outside [0, A)
+    auto word_mask = [&](int lo) -> uint32_t {   // lo = record byte of the word's byte 0
+        uint32_t m = 0xFFFFFFFFu;
+        if (lo < 0) m = lo <= -4 ? 0u : m << (8 * (-lo));
+        if (lo + 4 > A) m = lo >= A ? 0u : m & (0xFFFFFFFFu >> (8 * (lo + 4 - A)));
+        return m;
+    };
+    auto chunk_at = [&](int i) -> uint4 {
+        uint4 v = w[i];
+        const int b0 = 16 * i - head;
+        if (b0 < 0 || b0 + 16 > A) {
+            v.x &= word_mask(b0); v.y &= word_mask(b0 + 4); v.z &= word_mask(b0 + 8); v.w &= word_mask(b0 + 12);
+        }
         return v;
     };
     int c = 0;
-    for (int i = w0; i < w1; i++) c += __popc(word_at(i));
+    for (int i = c0; i < c1; i++) c += chunk_count_bytes(chunk_at(i));
     int incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -113,12 +127,20 @@ __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A,
     int64_t act = -1;
     if (d >= excl && d < incl) {
         int r = d - excl;
-        for (int i = w0; i < w1; i++) {
-            uint32_t v = word_at(i);
-            const int pc = __popc(v);
+        for (int i = c0; i < c1; i++) {
+            const uint4 v = chunk_at(i);
+            const int pc = chunk_count_bytes(v);
             if (r < pc) {
-                for (; r > 0; r--) v &= v - 1;
-                act = 4 * i + ((__ffs(v) - 1) >> 3) - head;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    uint32_t y = (k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w) & 0x01010101u;
+                    const int q = __popc(y);
+                    if (act < 0 && r < q) {
+                        for (; r > 0; r--) y &= y - 1;
+                        act = 16 * i + 4 * k + ((__ffs(y) - 1) >> 3) - head;
+                    }
+                    r -= q;
+                }
                 break;
             }
             r -= pc;
