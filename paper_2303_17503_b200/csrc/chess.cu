@@ -400,10 +400,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         if (reset) {
             int c = (int)(child(k, 0) % 2ull);
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
-            const uint8_t back[8] = {R, N, B, Q, K, B, N, R};
+            constexpr uint32_t back = 0x42365324u;   // R N B Q K B N R, nibble f = file f
             for (int s = lane; s < 64; s += 32) {
                 int r = s >> 3, f = s & 7;
-                uint8_t v = r == 0 ? mk(0, back[f]) : r == 1 ? mk(0, P) : r == 6 ? mk(1, P) : r == 7 ? mk(1, back[f]) : 0;
+                const int bk = (int)((back >> (4 * f)) & 15u);
+                uint8_t v = r == 0 ? mk(0, bk) : r == 1 ? mk(0, P) : r == 6 ? mk(1, P) : r == 7 ? mk(1, bk) : 0;
                 S.bd[s] = v;
             }
             stm = 0; castle = 15; ep = -1; halfmove = 0; step = 0;
@@ -593,21 +594,26 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         for (int pass = 0; pass < 2; pass++) {
             const int v = 2 * lane + pass;
             const int sabs = v ^ fl;
-            uint32_t w[4] = {0u, 0u, 0u, 0u};   // 119-bit pattern of square v (bit k = plane k)
+            // 119-bit pattern of square v (bit k = plane k) in two registers
+            uint64_t plo = 0ull, phi = 0ull;
 #pragma unroll
             for (int t = 0; t < 8; t++) {
-                uint8_t pc = S.past[t][sabs];
-                int base = 14 * t;
+                const uint8_t pc = S.past[t][sabs];
+                const int base = 14 * t;
                 if (pc) {
-                    int bit = base + (color(pc) == side ? 0 : 6) + type(pc) - 1;
-                    w[bit >> 5] |= 1u << (bit & 31);
+                    const int bit = base + (color(pc) == side ? 0 : 6) + type(pc) - 1;
+                    plo |= bit < 64 ? 1ull << bit : 0ull;
+                    phi |= bit >= 64 ? 1ull << (bit - 64) : 0ull;
                 }
-                uint8_t rp = S.prep[t];
-                if (rp >= 1) w[(base + 12) >> 5] |= 1u << ((base + 12) & 31);
-                if (rp >= 2) w[(base + 13) >> 5] |= 1u << ((base + 13) & 31);
+                const uint8_t rp = S.prep[t];
+                const uint64_t r1 = rp >= 1 ? 1ull : 0ull, r2 = rp >= 2 ? 1ull : 0ull;
+                if (base + 13 < 64) plo |= (r1 << (base + 12)) | (r2 << (base + 13));
+                else if (base + 12 >= 64) phi |= (r1 << (base + 12 - 64)) | (r2 << (base + 13 - 64));
+                else { plo |= r1 << (base + 12); phi |= r2 << (base + 13 - 64); }
             }
             // planes 112.. : colour, [113 count], castling x4, [118 count]
-            w[3] |= cbits << (112 - 96);
+            phi |= (uint64_t)cbits << (112 - 64);
+            const uint32_t w[4] = {(uint32_t)plo, (uint32_t)(plo >> 32), (uint32_t)phi, (uint32_t)(phi >> 32)};
             // OR the 119-bit pattern into the stream at bit offset 119 v
             const int off = 119 * v, wi = off >> 5, sh = off & 31;
 #pragma unroll
@@ -624,7 +630,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             // 64 squares as scalar stores, ordered after the vector stores by __syncwarp
             float* orec = p.out.observation + b * (int64_t)NF;
             float4* o4 = reinterpret_cast<float4*>(orec);
-            for (int j = lane; j < NF / 4; j += 32) o4[j] = lut[(S.bits[j >> 3] >> ((j & 7) * 4)) & 15u];
+            // chunk j = lane + 32 m: word lane / 8 + 4 m, lane-constant nibble (lane % 8)
+            const uint32_t* wp = S.bits + (lane >> 3);
+            const uint32_t nsh = (uint32_t)(lane & 7) * 4u;
+#pragma unroll 4
+            for (int j = lane; j < NF / 4; j += 32, wp += 4) o4[j] = lut[(*wp >> nsh) & 15u];
             __syncwarp();
             const float cnt113 = (float)step / 512.0f, cnt118 = (float)halfmove / 100.0f;
             orec[119 * lane + 113] = cnt113;
