@@ -55,6 +55,11 @@ struct WarpSmem {
     uint8_t kesc[8];           // own king: neighbour d is a legal king destination
     uint64_t pinray[8][2];     // 81-bit ray masks (lo 64 | hi 17)
     int8_t pinsq[8];
+    uint8_t hand[16];          // hands [2][7] (absolute owners)
+    // next-board prefetch (cp.async): board, misc, repetition Bloom filter
+    alignas(16) uint8_t pf_abs[96];
+    alignas(16) uint8_t pf_misc[16];
+    alignas(16) uint32_t pf_bloom[2 * BLOOM_U64];
 };
 
 struct Params {
@@ -204,32 +209,26 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
         }
     }
     if (in_check) hp |= 1ull << (118 - 62);
-    uint32_t cpat[4];   // bits 62..118 of a 128-bit record pattern
-    cpat[0] = 0u;
-    cpat[1] = (uint32_t)(hp << 30);            // bits 62,63
-    cpat[2] = (uint32_t)(hp >> 2);
-    cpat[3] = (uint32_t)(hp >> 34);
     for (int pass = 0; pass < 4; pass++) {
         const int s = pass < 2 ? 2 * lane + pass : 64 + 2 * lane + (pass - 2);
         if (s < 81) {
-            uint32_t w[4] = {cpat[0], cpat[1], cpat[2], cpat[3]};
+            // 119-bit pattern of square s in two registers: piece (bit 31 owner + type - 1),
+            // attacker types at 14 / 45, attacker-count thresholds at 28-30 / 59-61, then
+            // the constant planes 62..118
+            uint64_t plo = hp << 62, phi = hp >> 2;
             const uint8_t pc = bd[s];
             if (pc) {
-                const int bit = 31 * owner(pc) + ptype(pc) - 1;
-                w[bit >> 5] |= 1u << (bit & 31);
+                const int bit = 31 * owner(pc) + ptype(pc) - 1;   // < 62
+                plo |= 1ull << bit;
             }
 #pragma unroll
             for (int who = 0; who < 2; who++) {
-                const uint32_t am = S.atk[who][s];
                 const int base = 31 * who + 14;
-                // 14 type bits at [base, base+14)
-                const uint64_t v = (uint64_t)am << (base & 31);
-                w[base >> 5] |= (uint32_t)v;
-                if ((base >> 5) + 1 < 4) w[(base >> 5) + 1] |= (uint32_t)(v >> 32);
-                const int n = S.acnt[who][s];
-                for (int q = 0; q < 3; q++)
-                    if (n > q) { const int bit = base + 14 + q; w[bit >> 5] |= 1u << (bit & 31); }
+                const uint32_t n = S.acnt[who][s];
+                const uint64_t thr = (n > 0 ? 1ull : 0ull) | (n > 1 ? 2ull : 0ull) | (n > 2 ? 4ull : 0ull);
+                plo |= ((uint64_t)S.atk[who][s] << base) | (thr << (base + 14));
             }
+            const uint32_t w[4] = {(uint32_t)plo, (uint32_t)(plo >> 32), (uint32_t)phi, (uint32_t)(phi >> 32)};
             const int off = 119 * s, wi = off >> 5, sh = off & 31;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -249,12 +248,43 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
             const uint32_t fi = lane < 4 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 4);
             rec[fi] = (float)((S.bits[fi >> 5] >> (fi & 31)) & 1u);
         }
+        // chunk j = lane + 32 m starts at bit head + 4 lane + 128 m: lane-constant shift
         float4* o4 = reinterpret_cast<float4*>(rec + head);
-        for (int j = lane; j < nchunk; j += 32) {
-            const uint32_t fi = (uint32_t)(head + 4 * j);
-            o4[j] = lut[__funnelshift_r(S.bits[fi >> 5], S.bits[(fi >> 5) + 1], fi & 31) & 15u];
-        }
+        const uint32_t q0 = (uint32_t)(head + 4 * lane), sh = q0 & 31u;
+        const uint32_t* wp = S.bits + (q0 >> 5);
+#pragma unroll 4
+        for (int j = lane; j < nchunk; j += 32, wp += 4) o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
     }
+}
+
+// One scalar field of board b per lane (lanes 0-3), loaded a board ahead.
+__device__ __forceinline__ uint64_t load_field(const Params& p, int64_t b, int lane) {
+    switch (lane) {
+        case 0: return (uint32_t)p.in.terminated[b] | ((uint32_t)p.in.truncated[b] << 8);
+        case 1: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
+        case 2: return (uint32_t)p.in.step_count[b];
+        case 3: return (uint64_t)p.actions[b];
+        default: return 0ull;
+    }
+}
+
+// cp.async board b's board, misc and repetition Bloom filter into the prefetch area.
+__device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int64_t b, int lane) {
+    const char* src = nullptr;
+    uint32_t dst = 0u;
+    if (lane < 6) {
+        src = reinterpret_cast<const char*>(p.in_s.board + b * BOARD_STRIDE) + 16 * lane;
+        dst = (uint32_t)__cvta_generic_to_shared(S.pf_abs) + 16u * lane;
+    } else if (lane == 6) {
+        src = reinterpret_cast<const char*>(p.in_s.misc + b * MISC);
+        dst = (uint32_t)__cvta_generic_to_shared(S.pf_misc);
+    } else if (lane < 7 + 16) {
+        const uint64_t* hist = p.out_s.hist + b * (int64_t)p.out_s.hist_cap;
+        src = reinterpret_cast<const char*>(hist + p.out_s.hist_cap - BLOOM_U64) + 16 * (lane - 7);
+        dst = (uint32_t)__cvta_generic_to_shared(S.pf_bloom) + 16u * (lane - 7);
+    }
+    if (src) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+    asm volatile("cp.async.commit_group;");
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
@@ -270,48 +300,58 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     const int cap = p.out_s.hist_cap;
     unsigned long long eps = 0;
-    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < p.n; b += nwarps) {
-        const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
+    uint8_t* hand = S.hand;
+    const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    uint64_t cur = 0ull;   // this board's scalar fields (lane j holds field j)
+    bool pf_ready = false;
+    for (int64_t b = b0; b < p.n; b += nwarps) {
+        if (!p.force_reset && !pf_ready) {   // first board of the warp: fetch synchronously
+            cur = load_field(p, b, lane);
+            issue_prefetch(S, p, b, lane);
+        }
+        const int64_t nb = b + nwarps;   // the next board's scalars are in flight meanwhile
+        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(p, nb, lane) : 0ull;
+        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0);
+        const bool reset = p.force_reset || (f_term & 0xFFFFu) != 0u;
+        if (!p.force_reset) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.out_s.hist + b * (int64_t)cap;
         int8_t p2r0, p2r1;
         int stm, step;
-        uint8_t hand[14];
         if (reset) {
             int c = (int)(child(k, 0) % 2ull);
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
             // lnsgkgsnl/1r5b1/ppppppppp/9/9/9/PPPPPPPPP/1B5R1/LNSGKGSNL (White = owner 1 at the top)
-            const uint8_t back[9] = {KY, KE, GI, KI, OU, KI, GI, KE, KY};
+            constexpr uint64_t back = 0x234585432ull;   // KY KE GI KI OU KI GI KE KY, nibble c = file c
             for (int s = lane; s < 96; s += 32) {
                 uint8_t v = 0;
                 if (s < 81) {
                     int r = s / 9, cc = s - 9 * r;
-                    if (r == 0) v = (uint8_t)(16 | back[cc]);
+                    const uint8_t bk = (uint8_t)((back >> (4 * cc)) & 15u);
+                    if (r == 0) v = (uint8_t)(16 | bk);
                     else if (r == 1) v = cc == 1 ? (uint8_t)(16 | HI) : cc == 7 ? (uint8_t)(16 | KA) : 0;
                     else if (r == 2) v = 16 | FU;
                     else if (r == 6) v = FU;
                     else if (r == 7) v = cc == 1 ? KA : cc == 7 ? HI : 0;
-                    else if (r == 8) v = back[cc];
+                    else if (r == 8) v = bk;
                 }
                 S.abs_[s] = v;
             }
-#pragma unroll
-            for (int j = 0; j < 14; j++) hand[j] = 0;
+            if (lane < 16) hand[lane] = 0;
             stm = 0; step = 0;
             __syncwarp();
         } else {
-            p2r0 = p.in.player_to_role[2 * b]; p2r1 = p.in.player_to_role[2 * b + 1];
-            const uint8_t* ib = p.in_s.board + b * BOARD_STRIDE;
-            for (int s = lane; s < 96; s += 32) S.abs_[s] = ib[s];
-            const uint8_t* m = p.in_s.misc + b * MISC;
-#pragma unroll
-            for (int j = 0; j < 14; j++) hand[j] = m[j];
-            stm = m[14];
-            step = p.in.step_count[b] + 1;
+            const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)cur, 1);
+            const int f_step = (int)__shfl_sync(BBK_FULL, (uint32_t)cur, 2);
+            const int f_act = (int)shfl64(cur, 3);
+            p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
+            for (int s = lane; s < 96; s += 32) S.abs_[s] = S.pf_abs[s];
+            if (lane < 16) hand[lane] = S.pf_misc[lane];
+            stm = S.pf_misc[14];
+            step = f_step + 1;
             __syncwarp();
-            if (lane == 0) apply_action(S.abs_, hand, stm, (int)p.actions[b]);
-#pragma unroll
-            for (int j = 0; j < 14; j++) hand[j] = (uint8_t)__shfl_sync(BBK_FULL, (int)hand[j], 0);
+            if (lane == 0) apply_action(S.abs_, hand, stm, f_act);
             stm ^= 1;
             __syncwarp();
         }
@@ -543,11 +583,18 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
             __syncwarp();
         }
         int reps = 0;
-        if (step > 0 && ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & 1u)) {
+        const uint32_t* pb = S.pf_bloom;   // prefetched copy of this env's filter
+        if (step > 0 && ((pb[i1 >> 5] >> (i1 & 31)) & (pb[i2 >> 5] >> (i2 & 31)) & 1u)) {
             for (int j = lane; j < step; j += 32) reps += hist[j] == key;
             reps = warp_sum(reps);
         }
-        __syncwarp();
+        __syncwarp();   // the prefetch area is free now: issue the next board's state
+        pf_ready = false;
+        if (!p.force_reset && nb < p.n) {
+            issue_prefetch(S, p, nb, lane);
+            cur = nxt;
+            pf_ready = true;
+        }
         if (lane == 0) {
             hist[step] = key;
             atomicOr(&bloom[i1 >> 5], 1u << (i1 & 31));
@@ -578,10 +625,10 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
         // ---- state + columns
         uint8_t* ob = p.out_s.board + b * BOARD_STRIDE;
         for (int s = lane; s < 96; s += 32) ob[s] = S.abs_[s];
+        if (lane < 14) p.out_s.misc[b * MISC + lane] = hand[lane];
         const int rep = reps > 3 ? 3 : reps;
         if (lane == 0) {
             uint8_t* m = p.out_s.misc + b * MISC;
-            for (int j = 0; j < 14; j++) m[j] = hand[j];
             m[14] = (uint8_t)side; m[15] = (uint8_t)rep;
             float r0 = 0.0f, r1 = 0.0f;
             if (!truncated && (rr0 != 0.0f || rr1 != 0.0f)) { r0 = p2r0 == 0 ? rr0 : rr1; r1 = p2r1 == 0 ? rr0 : rr1; }
