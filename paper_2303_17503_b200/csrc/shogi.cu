@@ -52,6 +52,9 @@ struct WarpSmem {
     uint8_t abs_[96];          // absolute board (state)
     uint16_t atk[2][81];       // attacking piece-type masks per owner
     uint8_t acnt[2][81];
+    // occupancy of every line: rows 0-8 (bit = column), columns 9-17 (bit = row),
+    // diagonals r - c = k - 8 at 18 + k and anti-diagonals r + c = k at 35 + k (bit = row)
+    uint16_t line[52];
     uint8_t kesc[8];           // own king: neighbour d is a legal king destination
     uint64_t pinray[8][2];     // 81-bit ray masks (lo 64 | hi 17)
     int8_t pinsq[8];
@@ -158,33 +161,56 @@ __device__ __forceinline__ uint64_t sq_key(uint8_t pc, int s) {
     return mix64(0x5306100000000000ULL + (uint64_t)pc * 128 + (uint64_t)s);
 }
 
+// Occupancy bit masks of the 52 lines of the board (one lane per line).
+__device__ void build_lines(WarpSmem& S, int lane) {
+    for (int j = lane; j < 52; j += 32) {
+        uint32_t m = 0u;
+#pragma unroll
+        for (int i = 0; i < 9; i++) {
+            const int r = j < 9 ? j : i;
+            const int c = j < 9 ? i : j < 18 ? j - 9 : j < 35 ? i - (j - 18) + 8 : (j - 35) - i;
+            if ((unsigned)c < 9u && S.bd[r * 9 + c]) m |= 1u << i;
+        }
+        S.line[j] = (uint16_t)m;
+    }
+}
+
 // Attack gather: for every target square, the piece types (14-bit mask) and
-// number of pieces of each owner attacking it (obs planes 14-30 / 45-61).
+// number of pieces of each owner attacking it (obs planes 14-30 / 45-61). The
+// first piece along each of the 8 rays comes from the line occupancy masks
+// (highest set bit below / lowest above the target's position), so there are
+// no data-dependent ray walks.
 __device__ void gather_attacks(WarpSmem& S, int lane) {
     const uint8_t* bd = S.bd;
     for (int t = lane; t < 81; t += 32) {
         const int r = t / 9, c = t - 9 * r;
-        uint16_t m0 = 0, m1 = 0;
-        uint8_t n0 = 0, n1 = 0;
+        uint32_t m0 = 0u, m1 = 0u, n0 = 0u, n1 = 0u;
+        const uint32_t Lrow = S.line[r], Lcol = S.line[9 + c], Ldia = S.line[18 + r - c + 8], Lant = S.line[35 + r + c];
+#pragma unroll
         for (int d = 0; d < 8; d++) {
-            int rr = r + DR[d], cc = c + DC[d], kk = 1;
-            while (son(rr, cc)) {
-                uint8_t pc = bd[rr * 9 + cc];
-                if (pc) {
-                    const int w = owner(pc), ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
-                    if (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) {
-                        if (w == 0) { m0 |= 1u << (ty - 1); n0++; } else { m1 |= 1u << (ty - 1); n1++; }
-                    }
-                    break;
-                }
-                rr += DR[d]; cc += DC[d]; kk++;
+            // line, position on it, and search side for direction d (DR/DC order)
+            const uint32_t L = d == 0 || d == 5 ? Lcol : d == 3 || d == 4 ? Lrow : d == 1 || d == 7 ? Ldia : Lant;
+            const int pos = d == 3 || d == 4 ? c : r;
+            const bool lower = d <= 3;   // UP, UP_LEFT, UP_RIGHT, LEFT: towards lower indices
+            const uint32_t m = lower ? L & ((1u << pos) - 1u) : L & ~((2u << pos) - 1u);
+            if (!m) continue;
+            const int bpos = lower ? 31 - __clz(m) : __ffs(m) - 1;
+            const int q = d == 3 || d == 4 ? r * 9 + bpos
+                        : d == 0 || d == 5 ? bpos * 9 + c
+                        : d == 1 || d == 7 ? bpos * 9 + (bpos - r + c)
+                                           : bpos * 9 + (r + c - bpos);
+            const bool adj = lower ? bpos == pos - 1 : bpos == pos + 1;
+            const uint8_t pc = bd[q];
+            const int w = owner(pc), ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
+            if (((adj ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) {
+                if (w == 0) { m0 |= 1u << (ty - 1); n0++; } else { m1 |= 1u << (ty - 1); n1++; }
             }
         }
         for (int dc = -1; dc <= 1; dc += 2) {
             if (son(r + 2, c + dc) && bd[(r + 2) * 9 + c + dc] == KE) { m0 |= 1u << (KE - 1); n0++; }
             if (son(r - 2, c + dc) && bd[(r - 2) * 9 + c + dc] == (16 | KE)) { m1 |= 1u << (KE - 1); n1++; }
         }
-        S.atk[0][t] = m0; S.atk[1][t] = m1; S.acnt[0][t] = n0; S.acnt[1][t] = n1;
+        S.atk[0][t] = (uint16_t)m0; S.atk[1][t] = (uint16_t)m1; S.acnt[0][t] = (uint8_t)n0; S.acnt[1][t] = (uint8_t)n1;
     }
 }
 
@@ -381,6 +407,8 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
             oksq = __shfl_sync(BBK_FULL, oksq, bo ? __ffs(bo) - 1 : 0);
             pawncols = __reduce_or_sync(BBK_FULL, pawncols);
         }
+        build_lines(S, lane);
+        __syncwarp();
         gather_attacks(S, lane);
         __syncwarp();
         const bool in_check = ksq >= 0 && S.acnt[1][ksq] > 0;
@@ -667,6 +695,8 @@ __global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st
         const uint8_t* m = st.misc + b * MISC;
 #pragma unroll
         for (int j = 0; j < 14; j++) hand[j] = m[j];
+        __syncwarp();
+        build_lines(S, lane);
         __syncwarp();
         gather_attacks(S, lane);
         int ksq = -1;
