@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="add a batch-size sweep 2^10..2^17 to the line")
+    ap.add_argument("--no-sweep", action="store_true", help="omit the batch-size sweep 2^10..2^17 from the line")
     ap.add_argument("--unfused", action="store_true", help="separate sampler / step / counter launches")
     return ap.parse_args()
 
@@ -252,7 +252,7 @@ def run_gpu(args, rank, world, local):
     }
     if not args.no_e2e:
         out["e2e"] = run_e2e(args, gdef, kern, root, dev, world, slot0, B)
-    if args.sweep:
+    if not args.no_sweep:
         out["sweep"] = run_sweep(args, gdef, kern, dev, slot0)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, game, B, args.cpu_seconds)
