@@ -188,6 +188,26 @@ int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int6
 int bbk_abi_version(void);
 const char* bbk_build_info(void);
 
+/* ------------------------------------------------- state fingerprints --
+ * Device-side core.state_fingerprint (core.py:417-434) for every slot of a
+ * batch: out[n, 16] = blake2b-16 of
+ *   game_id | <iiBB>(current_player, step_count, terminated, truncated)
+ *   | player_to_role | rewards f32[2] | packbits(mask, MSB first) | Core.encode().
+ * `scratch` is [n, stride] bytes (stride = bbk_fingerprint_stride), `lens` [n].
+ * batch_fingerprint (core.py:437-441) is blake2b over out[0..n) in slot order.
+ * game_code: 0 Go (size = board size), 1 backgammon, 2 chess, 3 shogi. */
+int bbk_fingerprint_stride(int game_code, int size);
+int bbk_go_fingerprint(int size, const bbk_cols* cols, const bbk_go_state* s, int64_t n, uint8_t* scratch,
+                       int64_t stride, int32_t* lens, uint8_t* out, void* stream);
+int bbk_bg_fingerprint(const bbk_cols* cols, const bbk_bg_state* s, int64_t n, uint8_t* scratch, int64_t stride,
+                       int32_t* lens, uint8_t* out, void* stream);
+int bbk_chess_fingerprint(const bbk_cols* cols, const bbk_chess_state* s, int64_t n, uint8_t* scratch,
+                          int64_t stride, int32_t* lens, uint8_t* out, void* stream);
+int bbk_shogi_fingerprint(const bbk_cols* cols, const bbk_shogi_state* s, int64_t n, uint8_t* scratch,
+                          int64_t stride, int32_t* lens, uint8_t* out, void* stream);
+/* Host build of the same blake2b-16 (pinned against hashlib by the CPU tests). */
+int bbk_blake2b16_host(const uint8_t* msg, int64_t len, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,8 +79,12 @@ def _declare(L):
             getattr(L, f"bbk_{g}_init").argtypes = [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P]
             getattr(L, f"bbk_{g}_step").argtypes = [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P]
             getattr(L, f"bbk_{g}_observe").argtypes = [ptr(S), P, P, P, I64, P]
-    for name in dir(L):
-        pass
+    L.bbk_fingerprint_stride.argtypes = [C.c_int, C.c_int]
+    L.bbk_go_fingerprint.argtypes = [C.c_int, ptr(Cols), ptr(GoState), I64, P, I64, P, P, P]
+    L.bbk_bg_fingerprint.argtypes = [ptr(Cols), ptr(BgState), I64, P, I64, P, P, P]
+    L.bbk_chess_fingerprint.argtypes = [ptr(Cols), ptr(ChessState), I64, P, I64, P, P, P]
+    L.bbk_shogi_fingerprint.argtypes = [ptr(Cols), ptr(ShogiState), I64, P, I64, P, P, P]
+    L.bbk_blake2b16_host.argtypes = [P, I64, P]
     return L
 
 

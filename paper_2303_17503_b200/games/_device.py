@@ -270,6 +270,22 @@ class DeviceKernel:
     def private_host(self, v: DeviceV) -> dict:
         return {k: t.cpu().numpy() for k, t in vars(v.priv).items()}
 
+    # -------------------------------------------------- device fingerprints
+    fp_code = -1   # bbk_fingerprint_stride game code
+
+    def fingerprints(self, v: DeviceV):
+        """core.state_fingerprint of every slot, computed on the device: uint8 [n, 16] (host)."""
+        torch = _torch()
+        stride = int(nat.lib().bbk_fingerprint_stride(self.fp_code, int(getattr(self, "size", 0))))
+        scratch = torch.empty((v.n, stride), dtype=torch.uint8, device=v.device)
+        lens = torch.empty(v.n, dtype=torch.int32, device=v.device)
+        out = torch.empty((v.n, 16), dtype=torch.uint8, device=v.device)
+        self.launch_fingerprint(v, scratch, stride, lens, out)
+        return out.cpu().numpy()
+
+    def launch_fingerprint(self, v, scratch, stride, lens, out) -> None:
+        raise NotImplementedError
+
     def state_at(self, gdef, v: DeviceV, i: int, limit: int) -> EnvState:
         s = self.host_snapshot(v)
         term = bool(s["terminated"][i])

@@ -53,6 +53,13 @@ class BackgammonKernel(DeviceKernel):
             return nat.BgState(nat.ptr(v.priv.points), nat.ptr(v.priv.misc))
         return nat.BgState(nat.ptr(v.priv.points[i:i + 1]), nat.ptr(v.priv.misc[i:i + 1]))
 
+    fp_code = 1
+
+    def launch_fingerprint(self, v, scratch, stride, lens, out) -> None:
+        nat.check(nat.lib().bbk_bg_fingerprint(self.cols(v), self.state_struct(v), v.n, nat.ptr(scratch), stride,
+                                               nat.ptr(lens), nat.ptr(out), nat.stream_handle(v.device)),
+                  "bbk_bg_fingerprint")
+
     def launch_init(self, v, ks, sk):
         nat.check(nat.lib().bbk_bg_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_bg_init")

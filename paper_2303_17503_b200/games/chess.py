@@ -91,6 +91,11 @@ class RingKernel(DeviceKernel):
         nat.check(fn(self.cols(v), self.state_struct(v), self.out_cols(out), self.state_struct(out), nat.ptr(a), v.n,
                      v.slot0, ks, nat.ptr(sk), limit, nat.stream_handle(v.device)), f"bbk_{self.prefix}_step")
 
+    def launch_fingerprint(self, v, scratch, stride, lens, out) -> None:
+        fn = getattr(nat.lib(), f"bbk_{self.prefix}_fingerprint")
+        nat.check(fn(self.cols(v), self.state_struct(v), v.n, nat.ptr(scratch), stride, nat.ptr(lens), nat.ptr(out),
+                     nat.stream_handle(v.device)), f"bbk_{self.prefix}_fingerprint")
+
     def launch_observe(self, v, i, roles, out):
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_observe")
         nat.check(fn(self.state_struct(v, i), nat.ptr(v.dev.step_count[i:i + 1]), nat.ptr(roles), nat.ptr(out), 1,
@@ -113,6 +118,7 @@ class RingKernel(DeviceKernel):
 class ChessKernel(RingKernel):
     game_id = "chess"
     prefix = "chess"
+    fp_code = 2
     num_actions = 4672
     obs_shape = (8, 8, 119)
     hist_bytes = HIST_BYTES

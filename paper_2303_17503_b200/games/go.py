@@ -137,6 +137,13 @@ class GoKernel(DeviceKernel):
                                         self.state_struct(out), out.store.struct(), nat.ptr(a), v.n, v.slot0, ks,
                                         nat.ptr(sk), limit, nat.stream_handle(v.device)), "bbk_go_step")
 
+    fp_code = 0
+
+    def launch_fingerprint(self, v, scratch, stride, lens, out) -> None:
+        nat.check(nat.lib().bbk_go_fingerprint(self.size, self.cols(v), self.state_struct(v), v.n, nat.ptr(scratch),
+                                               stride, nat.ptr(lens), nat.ptr(out), nat.stream_handle(v.device)),
+                  "bbk_go_fingerprint")
+
     def launch_observe(self, v, i, roles, out) -> None:
         nat.check(nat.lib().bbk_go_observe(self.size, nat.ptr(v.priv.pat[i:i + 1]), nat.ptr(roles), nat.ptr(out), 1,
                                            nat.stream_handle(v.device)), "bbk_go_observe")

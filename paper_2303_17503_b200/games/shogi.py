@@ -39,6 +39,7 @@ class ShogiCoreView:
 class ShogiKernel(RingKernel):
     game_id = "shogi"
     prefix = "shogi"
+    fp_code = 3
     num_actions = 2187
     obs_shape = (9, 9, 119)
     board_bytes = 96
