@@ -1,5 +1,6 @@
 """Host-side API contract (no GPU): registry, specs, errors, key schedule (reference test_core.py:10-50)."""
 
+import numpy as np
 import pytest
 
 import paper_2303_17503_b200 as bb
@@ -61,3 +62,26 @@ def test_session_key_schedule_matches_reference_formula():
     root = bb.RngKey(0)
     assert root.child(0).state != root.child(1).state
     assert bb.RngKey(0).state == 0xE220A8397B1DCDAF
+
+
+def test_output_wire_parser_roundtrip():
+    """unpack_outputs reads the binary batch-outputs format (header + 64-B aligned fields)."""
+    import json
+    import struct
+
+    from paper_2303_17503_b200.session import _WIRE_MAGIC, unpack_outputs
+
+    a = np.arange(6, dtype=np.float32).reshape(2, 3)
+    m = np.array([[True, False]], dtype=bool)
+    hdr = json.dumps({"game_id": "x", "n": 2, "fields": {"observations": ["float32", [2, 3], 0, 24],
+                                                         "legal_action_mask": ["bool", [1, 2], 64, 2]}}).encode()
+    pre = _WIRE_MAGIC + struct.pack("<I", len(hdr)) + hdr
+    base = (len(pre) + 63) // 64 * 64
+    buf = bytearray(base + 66)
+    buf[:len(pre)] = pre
+    buf[base:base + 24] = a.tobytes()
+    buf[base + 64:base + 66] = m.tobytes()
+    o = unpack_outputs(bytes(buf))
+    assert np.array_equal(o["observations"], a) and np.array_equal(o["legal_action_mask"], m)
+    with pytest.raises(ValueError):
+        unpack_outputs(b"XXXX" + bytes(60))
