@@ -188,6 +188,24 @@ int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int6
 int bbk_abi_version(void);
 const char* bbk_build_info(void);
 
+/* ------------------------------------------------------- small engines --
+ * The reference's other engines, one thread per slot:
+ * game 0 tic_tac_toe (games/tictactoe.py), 1 connect_four (connect_four.py),
+ * 2 othello (othello.py), 3 hex (hexgame.py), 4 2048 (play2048.py),
+ * 5 kuhn_poker (kuhn_poker.py), 6 leduc_holdem (leduc_holdem.py).
+ * Per-slot Core in a BBK_SMALL_STATE_BYTES blob [n, 48] (layouts in
+ * csrc/small.cuh). Columns as above, except that the one-player 2048 has
+ * rewards [n, 1] and player_to_role [n, 1]. */
+#define BBK_SMALL_STATE_BYTES 48
+int bbk_small_state_bytes(void);
+int bbk_small_init(int game, const bbk_cols* out, uint8_t* out_blob, int64_t n, int64_t slot0, uint64_t key_state,
+                   const uint64_t* slot_keys, int32_t max_steps, void* stream);
+int bbk_small_step(int game, const bbk_cols* in, const uint8_t* in_blob, const bbk_cols* out, uint8_t* out_blob,
+                   const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
+                   int32_t max_steps, void* stream);
+int bbk_small_observe(int game, const uint8_t* blob, const uint8_t* terminated, const uint8_t* role, float* obs,
+                      int64_t n, void* stream);
+
 /* ------------------------------------------------- state fingerprints --
  * Device-side core.state_fingerprint (core.py:417-434) for every slot of a
  * batch: out[n, 16] = blake2b-16 of
@@ -195,7 +213,7 @@ const char* bbk_build_info(void);
  *   | player_to_role | rewards f32[2] | packbits(mask, MSB first) | Core.encode().
  * `scratch` is [n, stride] bytes (stride = bbk_fingerprint_stride), `lens` [n].
  * batch_fingerprint (core.py:437-441) is blake2b over out[0..n) in slot order.
- * game_code: 0 Go (size = board size), 1 backgammon, 2 chess, 3 shogi. */
+ * game_code: 0 Go (size = board size), 1 backgammon, 2 chess, 3 shogi, 4 small engines. */
 int bbk_fingerprint_stride(int game_code, int size);
 int bbk_go_fingerprint(int size, const bbk_cols* cols, const bbk_go_state* s, int64_t n, uint8_t* scratch,
                        int64_t stride, int32_t* lens, uint8_t* out, void* stream);
@@ -204,6 +222,8 @@ int bbk_bg_fingerprint(const bbk_cols* cols, const bbk_bg_state* s, int64_t n, u
 int bbk_chess_fingerprint(const bbk_cols* cols, const bbk_chess_state* s, int64_t n, uint8_t* scratch,
                           int64_t stride, int32_t* lens, uint8_t* out, void* stream);
 int bbk_shogi_fingerprint(const bbk_cols* cols, const bbk_shogi_state* s, int64_t n, uint8_t* scratch,
+                          int64_t stride, int32_t* lens, uint8_t* out, void* stream);
+int bbk_small_fingerprint(int game, const bbk_cols* cols, const uint8_t* blob, int64_t n, uint8_t* scratch,
                           int64_t stride, int32_t* lens, uint8_t* out, void* stream);
 /* Host build of the same blake2b-16 (pinned against hashlib by the CPU tests). */
 int bbk_blake2b16_host(const uint8_t* msg, int64_t len, uint8_t* out);

@@ -85,6 +85,10 @@ def _declare(L):
     L.bbk_chess_fingerprint.argtypes = [ptr(Cols), ptr(ChessState), I64, P, I64, P, P, P]
     L.bbk_shogi_fingerprint.argtypes = [ptr(Cols), ptr(ShogiState), I64, P, I64, P, P, P]
     L.bbk_blake2b16_host.argtypes = [P, I64, P]
+    L.bbk_small_fingerprint.argtypes = [C.c_int, ptr(Cols), P, I64, P, I64, P, P, P]
+    L.bbk_small_init.argtypes = [C.c_int, ptr(Cols), P, I64, I64, U64, P, I32, P]
+    L.bbk_small_step.argtypes = [C.c_int, ptr(Cols), P, ptr(Cols), P, P, I64, I64, U64, P, I32, P]
+    L.bbk_small_observe.argtypes = [C.c_int, P, P, P, P, I64, P]
     return L
 
 

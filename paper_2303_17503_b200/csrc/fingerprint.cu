@@ -13,6 +13,7 @@
 // batch_fingerprint (core.py:437-441) is blake2b over the per-slot digests in
 // slot order, done by the host over n x 16 bytes.
 #include "common.cuh"
+#include "small.cuh"
 #include "../../include/bbk.h"
 
 namespace fp {
@@ -117,16 +118,14 @@ struct Writer {
 };
 
 // game id, scalar fields, rewards and the MSB-first packed legal mask (core.py:421-426)
-__device__ void write_prefix(Writer& w, const char* gid, const bbk_cols& c, int64_t b, int A) {
+__device__ void write_prefix(Writer& w, const char* gid, const bbk_cols& c, int64_t b, int A, int P = 2) {
     w.str(gid);
     w.u32((uint32_t)c.current_player[b]);
     w.u32((uint32_t)c.step_count[b]);
     w.u8(c.terminated[b] ? 1u : 0u);
     w.u8(c.truncated[b] ? 1u : 0u);
-    w.u8((uint8_t)c.player_to_role[2 * b]);
-    w.u8((uint8_t)c.player_to_role[2 * b + 1]);
-    w.u32(__float_as_uint(c.rewards[2 * b]));
-    w.u32(__float_as_uint(c.rewards[2 * b + 1]));
+    for (int q = 0; q < P; q++) w.u8((uint8_t)c.player_to_role[P * b + q]);
+    for (int q = 0; q < P; q++) w.u32(__float_as_uint(c.rewards[P * b + q]));
     const uint8_t* m = c.legal_action_mask + b * (int64_t)A;
     for (int j = 0; j < (A + 7) / 8; j++) {
         uint32_t byte = 0;
@@ -210,6 +209,20 @@ __global__ void shogi_msg_kernel(bbk_cols c, bbk_shogi_state s, int64_t n, uint8
     lens[b] = w.n;
 }
 
+template <class G>
+__global__ void small_msg_kernel(int game, bbk_cols c, const uint8_t* blob, int64_t n,
+                                 uint8_t* msgs, int64_t stride, int32_t* lens) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const char* ids[7] = {"tic_tac_toe", "connect_four", "othello", "hex", "2048", "kuhn_poker", "leduc_holdem"};
+    Writer w{msgs + b * stride, 0};
+    write_prefix(w, ids[game], c, b, G::A, G::P);
+    small::St s;
+    for (int i = 0; i < small::kStateBytes; i++) s.b[i] = blob[b * small::kStateBytes + i];
+    G::encode(s, w);   // the engine's Core.encode
+    lens[b] = w.n;
+}
+
 __global__ void hash_kernel(const uint8_t* msgs, int64_t stride, const int32_t* lens, int64_t n, uint8_t* out) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n) return;
@@ -238,7 +251,8 @@ int bbk_fingerprint_stride(int game_code, int size) {
         case 0: { const int C = size * size; A = C + 1; enc = C + 2 + 8 + 8 + 2 + 8 * C; break; }
         case 1: A = 156; enc = 24 + 7 + 4; break;
         case 2: A = 4672; enc = 64 + 5; break;
-        default: A = 2187; enc = 81 + 16; break;
+        case 3: A = 2187; enc = 81 + 16; break;
+        default: A = 128; enc = 64; break;   // small engines (game_code 10 + bbk_small game)
     }
     return ((16 + 10 + 2 + 8 + (A + 7) / 8 + enc) + 15) & ~15;
 }
@@ -273,6 +287,27 @@ int bbk_shogi_fingerprint(const bbk_cols* c, const bbk_shogi_state* s, int64_t n
     const bbk_shogi_state ss = *s;
     return fp::run([&](unsigned g, cudaStream_t st) { fp::shogi_msg_kernel<<<g, 128, 0, st>>>(cc, ss, n, scratch, stride, lens); },
                    scratch, stride, lens, n, out, (cudaStream_t)stream);
+}
+
+int bbk_small_fingerprint(int game, const bbk_cols* c, const uint8_t* blob, int64_t n, uint8_t* scratch,
+                          int64_t stride, int32_t* lens, uint8_t* out, void* stream) {
+    const bbk_cols cc = *c;
+    auto go = [&](auto g) {
+        using G = decltype(g);
+        return fp::run([&](unsigned gr, cudaStream_t st) {
+            fp::small_msg_kernel<G><<<gr, 128, 0, st>>>(game, cc, blob, n, scratch, stride, lens);
+        }, scratch, stride, lens, n, out, (cudaStream_t)stream);
+    };
+    switch (game) {
+        case 0: return go(small::TicTacToe{});
+        case 1: return go(small::ConnectFour{});
+        case 2: return go(small::Othello{});
+        case 3: return go(small::Hex{});
+        case 4: return go(small::Play2048{});
+        case 5: return go(small::Kuhn{});
+        case 6: return go(small::Leduc{});
+        default: return (int)cudaErrorInvalidValue;
+    }
 }
 
 // Host build of the same blake2b (CPU tests pin it against hashlib).

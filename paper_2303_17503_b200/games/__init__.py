@@ -1,17 +1,20 @@
 """Device engines and the game registry (reference games/__init__.py:1-36).
 
 Registered here: the north-star games go_9x9, go_19x19, backgammon, chess,
-shogi. The reference's other engines and reserved ids keep their metadata
-(``game_spec`` works) and raise ``UnsupportedGame`` on use: they are outside
-this build's hot-path scope.
+shogi, and the reference's small engines (tic_tac_toe, connect_four,
+othello, hex, 2048, kuhn_poker, leduc_holdem; games/small.py). The
+remaining reserved ids keep their metadata (``game_spec`` works) and raise
+``UnsupportedGame`` on use.
 """
 
 from ..core import GameSpec, register, reserve
-from . import backgammon, go
+from . import backgammon, go, small
 
 register(go.GAME)
 register(go.GAME19)
 register(backgammon.GAME)
+for _g in small.GAMES:
+    register(_g)
 
 try:
     from . import chess as _chess

@@ -125,6 +125,7 @@ class DeviceKernel:
 
     game_id = ""
     num_actions = 0
+    num_players = 2
     obs_shape: tuple = ()
 
     # ------------------------------------------------------------ allocation
@@ -134,12 +135,12 @@ class DeviceKernel:
         d = v.dev
         d.observation = torch.empty((n,) + tuple(self.obs_shape), dtype=torch.float32, device=device) if obs else None
         d.legal_action_mask = torch.empty((n, self.num_actions), dtype=torch.bool, device=device)
-        d.rewards = torch.empty((n, 2), dtype=torch.float32, device=device)
+        d.rewards = torch.empty((n, self.num_players), dtype=torch.float32, device=device)
         d.terminated = torch.empty(n, dtype=torch.bool, device=device)
         d.truncated = torch.empty(n, dtype=torch.bool, device=device)
         d.current_player = torch.empty(n, dtype=torch.int32, device=device)
         d.step_count = torch.empty(n, dtype=torch.int32, device=device)
-        d.player_to_role = torch.empty((n, 2), dtype=torch.int8, device=device)
+        d.player_to_role = torch.empty((n, self.num_players), dtype=torch.int8, device=device)
         self.alloc_private(v)
         return v
 
@@ -294,7 +295,7 @@ class DeviceKernel:
         rewards.flags.writeable = False
         mask = s["legal_action_mask"][i].copy()
         mask.flags.writeable = False
-        p2r = (int(s["player_to_role"][i, 0]), int(s["player_to_role"][i, 1]))
+        p2r = tuple(int(x) for x in s["player_to_role"][i])
         core = self.core_view(s, i, p2r, rewards, mask, term)
         return EnvState(
             current_player=int(s["current_player"][i]),
@@ -316,8 +317,8 @@ class DeviceKernel:
 
     @staticmethod
     def role_rewards(p2r, rewards) -> tuple:
-        rr = [0.0, 0.0]
-        for p in range(2):
+        rr = [0.0] * len(p2r)
+        for p in range(len(p2r)):
             rr[p2r[p]] = float(rewards[p])
         return tuple(rr)
 

@@ -11,12 +11,13 @@ import paper_2303_17503_b200 as bb
 pytestmark = pytest.mark.gpu
 
 GAMES = ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"]
+SMALL = ["tic_tac_toe", "connect_four", "othello", "hex", "2048", "kuhn_poker", "leduc_holdem"]
 
 
-@pytest.mark.parametrize("game", GAMES)
+@pytest.mark.parametrize("game", GAMES + SMALL)
 def test_device_fingerprints_equal_host(game):
     # short episodes so that finished / reset slots and long Go histories all occur
-    max_steps = {"go_9x9": 40, "go_19x19": 12, "backgammon": 60, "chess": 30, "shogi": 30}[game]
+    max_steps = {"go_9x9": 40, "go_19x19": 12, "backgammon": 60, "chess": 30, "shogi": 30}.get(game, 20)
     sess = bb.BatchSession(game, 96, 5, max_steps=max_steps)
     for t in range(max_steps + 7):
         sess.step(sess.sample_random_actions())

@@ -150,13 +150,13 @@ def test_env_core_contract_all_games():                # test_core.py:52-84
         assert not state.terminated and not state.truncated and state.step_count == 0
         assert state.legal_action_mask.shape == (spec.num_actions,) and state.legal_action_mask.any()
         assert np.all(state.rewards == 0)
-        assert sorted(state.player_to_role) == [0, 1]
+        assert sorted(state.player_to_role) == list(range(spec.num_players))
         assert state.player_to_role[state.current_player] == state.core.role_to_move
-        for p in range(2):
+        for p in range(spec.num_players):
             obs = bb.observe(state, p)
             assert obs.shape == spec.observation_shape and obs.dtype == np.float32
         with pytest.raises(bb.InvalidPlayer):
-            bb.observe(state, 2)
+            bb.observe(state, spec.num_players)
 
 
 def test_pgx_style_facade():

@@ -12,10 +12,18 @@ EXPECTED = {
     "backgammon": (2, (34,), 156),
     "chess": (2, (8, 8, 119), 4672),
     "shogi": (2, (9, 9, 119), 2187),
+    # the reference's small engines (games/*.py specs)
+    "tic_tac_toe": (2, (3, 3, 2), 9),
+    "connect_four": (2, (6, 7, 2), 7),
+    "othello": (2, (8, 8, 2), 65),
+    "hex": (2, (11, 11, 4), 122),
+    "2048": (1, (4, 4, 31), 4),
+    "kuhn_poker": (2, (7,), 4),
+    "leduc_holdem": (2, (34,), 3),
 }
 
 
-def test_registry_has_the_five_hot_path_games():
+def test_registry_has_the_hot_path_and_small_games():
     assert set(bb.available_games()) == set(EXPECTED)
 
 
@@ -26,7 +34,7 @@ def test_specs_match_table(game_id):
 
 
 def test_reserved_and_unknown_ids():
-    for game_id in ("tic_tac_toe", "othello", "animal_shogi", "minatar_breakout"):
+    for game_id in ("gardner_chess", "bridge_bidding", "animal_shogi", "minatar_breakout"):
         assert bb.game_spec(game_id).num_actions > 0
         with pytest.raises(bb.UnsupportedGame):
             bb.batch_init(game_id, bb.RngKey(0), 2)
