@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define BBK_ABI_VERSION 2
+#define BBK_ABI_VERSION 3   /* 3: bbk_go_state.lab, fingerprints, small engines */
 
 typedef struct bbk_cols {
     float*    observation;        /* may be NULL: skip observation emission */

@@ -59,36 +59,47 @@ class ShogiState(C.Structure):
 
 
 def _declare(L):
+    """ctypes signatures. A symbol missing from an older library build (A/B runs with BBK_LIB)
+    is skipped here; tests/test_abi.py checks that the in-tree build exports all of include/bbk.h."""
     ptr = C.POINTER
-    L.bbk_abi_version.restype = C.c_int
-    L.bbk_build_info.restype = C.c_char_p
-    L.bbk_go_pat_stride.argtypes = [C.c_int]
-    L.bbk_go_init.argtypes = [C.c_int, ptr(Cols), ptr(GoState), ptr(GoStore), I64, I64, U64, P, I32, P]
-    L.bbk_go_step.argtypes = [C.c_int, C.c_double, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
-                              P, I64, I64, U64, P, I32, P]
-    L.bbk_go_observe.argtypes = [C.c_int, P, P, P, I64, P]
-    L.bbk_go_rebuild_bloom.argtypes = [ptr(GoStore), P, I64, P]
-    L.bbk_bg_init.argtypes = [ptr(Cols), ptr(BgState), I64, I64, U64, P, I32, P]
-    L.bbk_bg_step.argtypes = [ptr(Cols), ptr(BgState), ptr(Cols), ptr(BgState), P, I64, I64, U64, P, I32, P]
-    L.bbk_bg_observe.argtypes = [ptr(BgState), P, P, I64, P]
-    L.bbk_random_actions.argtypes = [P, I64, I32, U64, I64, P, P]
-    L.bbk_check_actions.argtypes = [P, P, P, P, I64, I32, P, P]
-    L.bbk_count_finished.argtypes = [P, P, I64, P, P]
+
+    def sig(name, argtypes=None, restype=None):
+        if not hasattr(L, name):
+            return
+        fn = getattr(L, name)
+        if argtypes is not None:
+            fn.argtypes = argtypes
+        if restype is not None:
+            fn.restype = restype
+
+    sig("bbk_abi_version", restype=C.c_int)
+    sig("bbk_build_info", restype=C.c_char_p)
+    sig("bbk_go_pat_stride", [C.c_int])
+    sig("bbk_go_init", [C.c_int, ptr(Cols), ptr(GoState), ptr(GoStore), I64, I64, U64, P, I32, P])
+    sig("bbk_go_step", [C.c_int, C.c_double, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
+                        P, I64, I64, U64, P, I32, P])
+    sig("bbk_go_observe", [C.c_int, P, P, P, I64, P])
+    sig("bbk_go_rebuild_bloom", [ptr(GoStore), P, I64, P])
+    sig("bbk_bg_init", [ptr(Cols), ptr(BgState), I64, I64, U64, P, I32, P])
+    sig("bbk_bg_step", [ptr(Cols), ptr(BgState), ptr(Cols), ptr(BgState), P, I64, I64, U64, P, I32, P])
+    sig("bbk_bg_observe", [ptr(BgState), P, P, I64, P])
+    sig("bbk_random_actions", [P, I64, I32, U64, I64, P, P])
+    sig("bbk_check_actions", [P, P, P, P, I64, I32, P, P])
+    sig("bbk_count_finished", [P, P, I64, P, P])
     for g, S in (("chess", ChessState), ("shogi", ShogiState)):
-        if hasattr(L, f"bbk_{g}_step"):
-            getattr(L, f"bbk_{g}_init").argtypes = [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P]
-            getattr(L, f"bbk_{g}_step").argtypes = [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P]
-            getattr(L, f"bbk_{g}_observe").argtypes = [ptr(S), P, P, P, I64, P]
-    L.bbk_fingerprint_stride.argtypes = [C.c_int, C.c_int]
-    L.bbk_go_fingerprint.argtypes = [C.c_int, ptr(Cols), ptr(GoState), I64, P, I64, P, P, P]
-    L.bbk_bg_fingerprint.argtypes = [ptr(Cols), ptr(BgState), I64, P, I64, P, P, P]
-    L.bbk_chess_fingerprint.argtypes = [ptr(Cols), ptr(ChessState), I64, P, I64, P, P, P]
-    L.bbk_shogi_fingerprint.argtypes = [ptr(Cols), ptr(ShogiState), I64, P, I64, P, P, P]
-    L.bbk_blake2b16_host.argtypes = [P, I64, P]
-    L.bbk_small_fingerprint.argtypes = [C.c_int, ptr(Cols), P, I64, P, I64, P, P, P]
-    L.bbk_small_init.argtypes = [C.c_int, ptr(Cols), P, I64, I64, U64, P, I32, P]
-    L.bbk_small_step.argtypes = [C.c_int, ptr(Cols), P, ptr(Cols), P, P, I64, I64, U64, P, I32, P]
-    L.bbk_small_observe.argtypes = [C.c_int, P, P, P, P, I64, P]
+        sig(f"bbk_{g}_init", [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P])
+        sig(f"bbk_{g}_step", [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P])
+        sig(f"bbk_{g}_observe", [ptr(S), P, P, P, I64, P])
+    sig("bbk_fingerprint_stride", [C.c_int, C.c_int])
+    sig("bbk_go_fingerprint", [C.c_int, ptr(Cols), ptr(GoState), I64, P, I64, P, P, P])
+    sig("bbk_bg_fingerprint", [ptr(Cols), ptr(BgState), I64, P, I64, P, P, P])
+    sig("bbk_chess_fingerprint", [ptr(Cols), ptr(ChessState), I64, P, I64, P, P, P])
+    sig("bbk_shogi_fingerprint", [ptr(Cols), ptr(ShogiState), I64, P, I64, P, P, P])
+    sig("bbk_blake2b16_host", [P, I64, P])
+    sig("bbk_small_fingerprint", [C.c_int, ptr(Cols), P, I64, P, I64, P, P, P])
+    sig("bbk_small_init", [C.c_int, ptr(Cols), P, I64, I64, U64, P, I32, P])
+    sig("bbk_small_step", [C.c_int, ptr(Cols), P, ptr(Cols), P, P, I64, I64, U64, P, I32, P])
+    sig("bbk_small_observe", [C.c_int, P, P, P, P, I64, P])
     return L
 
 

@@ -58,6 +58,8 @@ struct WarpSmem {
     uint8_t kesc[8];           // own king: neighbour d is a legal king destination
     uint64_t pinray[8][2];     // 81-bit ray masks (lo 64 | hi 17)
     int8_t pinsq[8];
+    int8_t pinidx[96];         // square -> index of the king ray that pins the piece on it, or -1
+    uint16_t task[320];        // own-piece move tasks: square | direction << 7 (8, 9 = knight jumps)
     uint8_t hand[16];          // hands [2][7] (absolute owners)
     // next-board prefetch (cp.async): board, misc, repetition Bloom filter
     alignas(16) uint8_t pf_abs[96];
@@ -388,6 +390,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
             S.bd[s] = v ? (uint8_t)((((v >> 4) ^ side) << 4) | (v & 15)) : (uint8_t)0;
         }
         for (int i = lane; i < (A + 48) / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = lane; i < 96 / 4; i += 32) reinterpret_cast<uint32_t*>(S.pinidx)[i] = 0xFFFFFFFFu;
         __syncwarp();
         const uint8_t* bd = S.bd;
         const int64_t mstart = b * (int64_t)A;
@@ -442,6 +445,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
                 rr += DR[d]; cc += DC[d]; kk++;
             }
             S.pinsq[d] = pin;
+            if (pin >= 0) S.pinidx[pin] = (int8_t)d;
             S.pinray[d][0] = pray.lo; S.pinray[d][1] = pray.hi;
             // king destination d: on board, not own, not attacked with the king lifted
             const int tr = kr + DR[d], tc = kc + DC[d];
@@ -475,44 +479,60 @@ __global__ void __launch_bounds__(kWarps * 32, 5) step_kernel(Params p) {
         if (nchecks == 0) { chk.lo = ~0ull; chk.hi = ~0ull; }
         else if (nchecks >= 2) { chk.lo = 0ull; chk.hi = 0ull; }
         __syncwarp();
-        // ---- moves of own pieces (lanes own squares)
+        // ---- moves of own pieces: (piece, direction) tasks strided over the lanes, so the
+        //      few pieces and their uneven rays do not serialise the warp
         int cnt = 0;
-        for (int s = lane; s < 81; s += 32) {
-            const uint8_t pc = bd[s];
-            if (!pc || owner(pc) != 0) continue;
-            const int ty = ptype(pc), r = s / 9, c = s - 9 * r;
-            if (ty == OU) {
-                for (int d = 0; d < 8; d++)
-                    if (S.kesc[d]) { mk[action_code(d, false, s + DR[d] * 9 + DC[d])] = 1; cnt++; }
-                continue;
-            }
-            M81 allow = chk;
+        if (lane < 8 && ksq >= 0 && S.kesc[lane]) {   // king destinations (lane = direction)
+            mk[action_code(lane, false, ksq + DR[lane] * 9 + DC[lane])] = 1;
+            cnt++;
+        }
+        {
+            uint32_t dirs[3];
+            int mine = 0;
 #pragma unroll
-            for (int d = 0; d < 8; d++)
-                if (S.pinsq[d] == s) { allow.lo &= S.pinray[d][0]; allow.hi &= S.pinray[d][1]; }
-            auto emit = [&](int d, int to) {
-                if (!allow.has(to)) return;
-                const int trow = to / 9;
-                const bool can_promo = promotable(ty) && (r <= 2 || trow <= 2);
-                const bool must = (ty == FU || ty == KY) ? trow == 0 : ty == KE ? trow <= 1 : false;
-                if (can_promo) { mk[action_code(d, true, to)] = 1; cnt++; }
-                if (!must) { mk[action_code(d, false, to)] = 1; cnt++; }
-            };
-            if (ty == KE) {
-                for (int j = 0; j < 2; j++) {
-                    const int rr = r - 2, cc = c + (j ? 1 : -1);
-                    if (!son(rr, cc)) continue;
-                    const uint8_t q = bd[rr * 9 + cc];
-                    if (q && owner(q) == 0) continue;
-                    emit(8 + j, rr * 9 + cc);
-                }
-                continue;
+            for (int j = 0; j < 3; j++) {
+                const int sq = lane + 32 * j;
+                const uint8_t pc = sq < 81 ? bd[sq] : (uint8_t)0;
+                const int ty = ptype(pc);
+                dirs[j] = (!pc || owner(pc) != 0 || ty == OU) ? 0u : ty == KE ? 0x300u : (uint32_t)(STEP[ty] | SLIDE[ty]);
+                mine += __popc(dirs[j]);
             }
-            const uint8_t st = STEP[ty], sl = SLIDE[ty];
-            for (int d = 0; d < 8; d++) {
-                if (!(((st | sl) >> d) & 1)) continue;
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(BBK_FULL, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int ntask = __shfl_sync(BBK_FULL, incl, 31);
+            int k = incl - mine;
+#pragma unroll
+            for (int j = 0; j < 3; j++)
+                for (uint32_t m = dirs[j]; m; m &= m - 1) S.task[k++] = (uint16_t)((lane + 32 * j) | ((__ffs(m) - 1) << 7));
+            __syncwarp();
+            for (int i = lane; i < ntask; i += 32) {
+                const int tk = S.task[i], sq = tk & 127, d = tk >> 7;
+                const int ty = ptype(bd[sq]), r = sq / 9, c = sq - 9 * (sq / 9);
+                M81 allow = chk;
+                const int pi = S.pinidx[sq];
+                if (pi >= 0) { allow.lo &= S.pinray[pi][0]; allow.hi &= S.pinray[pi][1]; }
+                auto emit = [&](int dd, int to) {
+                    if (!allow.has(to)) return;
+                    const int trow = to / 9;
+                    const bool can_promo = promotable(ty) && (r <= 2 || trow <= 2);
+                    const bool must = (ty == FU || ty == KY) ? trow == 0 : ty == KE ? trow <= 1 : false;
+                    if (can_promo) { mk[action_code(dd, true, to)] = 1; cnt++; }
+                    if (!must) { mk[action_code(dd, false, to)] = 1; cnt++; }
+                };
+                if (d >= 8) {   // knight jump (-2, -1) / (-2, +1)
+                    const int rr = r - 2, cc = c + (d == 9 ? 1 : -1);
+                    if (son(rr, cc)) {
+                        const uint8_t q = bd[rr * 9 + cc];
+                        if (!(q && owner(q) == 0)) emit(d, rr * 9 + cc);
+                    }
+                    continue;
+                }
+                const bool slide = (SLIDE[ty] >> d) & 1;
                 int rr = r + DR[d], cc = c + DC[d];
-                const bool slide = (sl >> d) & 1;
                 while (son(rr, cc)) {
                     const int to = rr * 9 + cc;
                     const uint8_t q = bd[to];
