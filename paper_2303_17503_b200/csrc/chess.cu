@@ -708,9 +708,8 @@ __global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, co
 }
 
 static int launch(const Params& p, cudaStream_t s) {
-    int64_t grid = (p.n + kWarps - 1) / kWarps;
-    if (grid > 148 * 12) grid = 148 * 12;
-    step_kernel<<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, 0, s>>>(p);
+    const int64_t grid = persistent_grid(step_kernel, kWarps * 32, 0, (p.n + kWarps - 1) / kWarps);
+    step_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -30,6 +30,20 @@ __device__ __forceinline__ uint64_t slot_key(const uint64_t* slot_keys, uint64_t
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Persistent grid: as many CTAs as fit on the device at once (the step kernels loop over
+// boards), so there is no partial second wave of CTAs.
+template <class Kernel>
+inline int64_t persistent_grid(Kernel kernel, int threads, size_t smem, int64_t need) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > need) grid = need;
+    return grid < 1 ? 1 : grid;
+}
+
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
     uint32_t lo = __shfl_sync(BBK_FULL, (uint32_t)v, src);
     uint32_t hi = __shfl_sync(BBK_FULL, (uint32_t)(v >> 32), src);

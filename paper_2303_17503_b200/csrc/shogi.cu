@@ -730,9 +730,8 @@ __global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st
 }
 
 static int launch(const Params& p, cudaStream_t s) {
-    int64_t grid = (p.n + kWarps - 1) / kWarps;
-    if (grid > 148 * 12) grid = 148 * 12;
-    step_kernel<<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, 0, s>>>(p);
+    const int64_t grid = persistent_grid(step_kernel, kWarps * 32, 0, (p.n + kWarps - 1) / kWarps);
+    step_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(p);
     return (int)cudaGetLastError();
 }
 
