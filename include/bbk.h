@@ -188,6 +188,13 @@ int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int6
 int bbk_abi_version(void);
 const char* bbk_build_info(void);
 
+/* Batched rollouts (agents.py:113-116 over a batch): after each step, record every slot's first
+ * finished episode -- returns [n, players] by player and its length -- into done / returns /
+ * lengths, and add the number of newly finished slots to *count. */
+int bbk_latch_finished(const uint8_t* terminated, const uint8_t* truncated, const float* rewards,
+                       const int32_t* step_count, int players, int64_t n, uint8_t* done, float* returns,
+                       int32_t* lengths, unsigned long long* count, void* stream);
+
 /* ------------------------------------------------------- small engines --
  * The reference's other engines, one thread per slot:
  * game 0 tic_tac_toe (games/tictactoe.py), 1 connect_four (connect_four.py),

@@ -86,6 +86,7 @@ def _declare(L):
     sig("bbk_random_actions", [P, I64, I32, U64, I64, P, P])
     sig("bbk_check_actions", [P, P, P, P, I64, I32, P, P])
     sig("bbk_count_finished", [P, P, I64, P, P])
+    sig("bbk_latch_finished", [P, P, P, P, C.c_int, I64, P, P, P, P, P])
     for g, S in (("chess", ChessState), ("shogi", ShogiState)):
         sig(f"bbk_{g}_init", [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P])
         sig(f"bbk_{g}_step", [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P])

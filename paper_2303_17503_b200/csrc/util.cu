@@ -2,6 +2,7 @@
 //   bbk_random_actions  -- agents.random_actions (reference agents.py:33-46)
 //   bbk_check_actions   -- IllegalAction detection (core.py:234-239, tictactoe.py:111-121)
 //   bbk_count_finished  -- episode counter of bench_run (bench.py:129)
+//   bbk_latch_finished  -- first-episode returns / lengths of a batched rollout (agents.py:113-116)
 #include "common.cuh"
 #include "../../include/bbk.h"
 
@@ -96,6 +97,23 @@ __global__ void count_finished_kernel(const uint8_t* term, const uint8_t* trunc,
     }
 }
 
+// Record each slot's first finished episode: returns by player and its length; count newly
+// finished slots (the host polls the count to stop the rollout).
+__global__ void latch_finished_kernel(const uint8_t* term, const uint8_t* trunc, const float* rewards,
+                                      const int32_t* step_count, int P, int64_t n, uint8_t* done, float* ret,
+                                      int32_t* len, unsigned long long* count) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool fresh = false;
+    if (b < n && !done[b] && (term[b] | trunc[b])) {
+        fresh = true;
+        done[b] = 1;
+        for (int q = 0; q < P; q++) ret[P * b + q] = rewards[P * b + q];
+        len[b] = step_count[b];
+    }
+    const unsigned m = __ballot_sync(BBK_FULL, fresh);
+    if (lane_id() == 0 && m) atomicAdd(count, (unsigned long long)__popc(m));
+}
+
 }  // namespace util
 
 extern "C" {
@@ -124,6 +142,15 @@ int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int6
     int64_t blocks = (n + 1023) / 1024;
     if (blocks > 148 * 4) blocks = 148 * 4;
     util::count_finished_kernel<<<(unsigned)blocks, 1024, 0, (cudaStream_t)stream>>>(terminated, truncated, n, count);
+    return (int)cudaGetLastError();
+}
+
+int bbk_latch_finished(const uint8_t* term, const uint8_t* trunc, const float* rewards, const int32_t* step_count,
+                       int players, int64_t n, uint8_t* done, float* returns, int32_t* lengths,
+                       unsigned long long* count, void* stream) {
+    if (n <= 0) return 0;
+    util::latch_finished_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        term, trunc, rewards, step_count, players, n, done, returns, lengths, count);
     return (int)cudaGetLastError();
 }
 
