@@ -285,10 +285,12 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
     t = 0
 
+    host_act.copy_(random_actions_device(batch, root.child(1)))
+
     def one():
+        # the host agent's actions (host_act, pinned) -> batch_step (H2D inside) -> D2H of the
+        # step's rewards / flags / current player and of the policy's next actions, one sync
         nonlocal batch, t
-        a = random_actions_device(batch, root.child(2 * t + 1))   # fused: produced by the previous launch
-        host_act.copy_(a)
         batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False,
                            next_key=root.child(2 * (t + 1) + 1))
         d = batch.device
@@ -296,6 +298,7 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
         host_f[:, 0].copy_(d.terminated, non_blocking=True)
         host_f[:, 1].copy_(d.truncated, non_blocking=True)
         host_cp.copy_(d.current_player, non_blocking=True)
+        host_act.copy_(random_actions_device(batch, root.child(2 * (t + 1) + 1)), non_blocking=True)
         torch.cuda.current_stream().synchronize()
         t += 1
 
@@ -315,7 +318,7 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
     return {"value": B * world * args.steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
-            "d2h_bytes_per_step": (8 + 8 + 2 + 4) * B, "steps": args.steps,
+            "d2h_bytes_per_step": (8 + 2 + 4 + 8) * B, "steps": args.steps,
             "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player, "
                     "same window as value (fresh init, W warm-up, K timed)"}
 
