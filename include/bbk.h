@@ -96,8 +96,9 @@ int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const 
                 int32_t max_steps, void* stream);
 
 /* batch_step (core.py:353-386): auto-reset of finished slots, else go.apply.
+ * allow_self_capture: make_game(allow_self_capture=True) (go.py:155-173, 249-255).
  * Actions are assumed legal (validate first with bbk_check_actions). */
-int bbk_go_step(int size, double komi, const bbk_cols* in, const bbk_go_state* in_s,
+int bbk_go_step(int size, double komi, int allow_self_capture, const bbk_cols* in, const bbk_go_state* in_s,
                 const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
                 const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state,
                 const uint64_t* slot_keys, int32_t max_steps, void* stream);

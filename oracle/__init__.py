@@ -240,11 +240,11 @@ def random_actions(mask: np.ndarray, key_state: int, slot0: int = 0) -> np.ndarr
     return actions.astype(np.int64)
 
 
-def make(game_id: str, n: int, max_steps: int | None = None) -> _Batch:
+def make(game_id: str, n: int, max_steps: int | None = None, self_capture: bool = False) -> _Batch:
     if game_id == "go_9x9":
-        return GoBatch(9, n, 512 if max_steps is None else max_steps)
+        return GoBatch(9, n, 512 if max_steps is None else max_steps, self_capture=self_capture)
     if game_id == "go_19x19":
-        return GoBatch(19, n, 512 if max_steps is None else max_steps)
+        return GoBatch(19, n, 512 if max_steps is None else max_steps, self_capture=self_capture)
     if game_id == "backgammon":
         return BackgammonBatch(n, 1024 if max_steps is None else max_steps)
     if game_id == "chess":
@@ -291,11 +291,12 @@ class ShogiBatch(_Batch):
 class Session:
     """BatchSession key schedule (reference bench.py:54-83) over an oracle batch."""
 
-    def __init__(self, game_id: str, n: int, seed: int, max_steps: int | None = None, slot0: int = 0):
+    def __init__(self, game_id: str, n: int, seed: int, max_steps: int | None = None, slot0: int = 0,
+                 self_capture: bool = False):
         from_seed = _mix64((seed + 0x9E3779B97F4A7C15) & ((1 << 64) - 1))
         self.root = from_seed
         self.slot0 = slot0
-        self.b = make(game_id, n, max_steps)
+        self.b = make(game_id, n, max_steps, self_capture)
         self.b.init(_child(self.root, 0), slot0)
         self.t = 0
 

@@ -76,7 +76,7 @@ def _declare(L):
     sig("bbk_build_info", restype=C.c_char_p)
     sig("bbk_go_pat_stride", [C.c_int])
     sig("bbk_go_init", [C.c_int, ptr(Cols), ptr(GoState), ptr(GoStore), I64, I64, U64, P, I32, P])
-    sig("bbk_go_step", [C.c_int, C.c_double, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
+    sig("bbk_go_step", [C.c_int, C.c_double, C.c_int, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
                         P, I64, I64, U64, P, I32, P])
     sig("bbk_go_observe", [C.c_int, P, P, P, I64, P])
     sig("bbk_go_rebuild_bloom", [ptr(GoStore), P, I64, P])

@@ -106,6 +106,7 @@ struct StepParams {
     int32_t max_steps;
     double komi;
     int force_reset;
+    int self_capture;   // make_game(allow_self_capture=True) (go.py:155-173, 249-255)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -189,7 +190,7 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 template <int N>
 __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y, uint32_t E, uint64_t h,
                                const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra,
-                               int nblack, int nwhite, int lane) {
+                               int nblack, int nwhite, bool self_capture, int lane) {
     constexpr uint32_t ROW = (1u << N) - 1u;
     auto& U = S.u.uf;
     const int r = lane;
@@ -287,6 +288,35 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     const uint32_t NAu = up_row(NA, lane), NAd = dn_row(NA, lane);
     const uint32_t nb = ((E << 1) | (E >> 1) | Eu | Ed | (NA << 1) | (NA >> 1) | NAu | NAd) & ROW;
     uint32_t cand = E & (capb | nb);
+    // Self-capture (go.py:155-173): an empty point whose own neighbours are all in atari on it
+    // (and that captures nothing) kills the merged group; the placed stone cancels in the hash,
+    // so h2 = h ^ XOR(zobrist of those chains), accumulated at the point in capx (free there:
+    // it is not a capture point). A lone stone would recreate h itself: superko rejects it.
+    uint32_t sc = 0u;
+    if (self_capture) {
+        const uint32_t Xn = ((X << 1) | (X >> 1) | up_row(X, lane) | dn_row(X, lane)) & ROW;
+        sc = E & ~capb & ~nb & Xn;
+        if (__any_sync(BBK_FULL, sc != 0u)) {
+            __syncwarp();
+            S.rcap[lane] = sc;
+            __syncwarp();
+            for (int i = lane; i < total; i += 32) {
+                const uint32_t e = U.run[i];
+                if (e >> 15) continue;   // mover's runs only
+                const uint32_t g = U.gst[U.root[i]];
+                if ((g & (g >> 10) & 0x3FFu) != 0u) continue;   // >= 2 liberties
+                const uint32_t lib = g & 0x3FFu;
+                if (!((S.rcap[lib / N] >> (lib % N)) & 1u)) continue;
+                const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
+                uint64_t x = 0ull;
+                for (int q = 0; q < len; q++) x ^= zkey<N>(rr * N + s + q, 1 - ycol);
+                uint32_t* cx = reinterpret_cast<uint32_t*>(&S.capx[lib]);
+                atomicXor(cx, (uint32_t)x);
+                atomicXor(cx + 1, (uint32_t)(x >> 32));
+            }
+            __syncwarp();
+        }
+    }
     uint32_t legal = 0u, pend = 0u;
     // one probe per board: if no history position had the stone counts a non-capture move
     // produces, none of those moves can repeat a position -> no hash / Bloom work for them
@@ -300,11 +330,12 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         legal = cand & ~capb;
         cand &= capb;
     }
+    cand |= sc;   // counts after a suicide are not known here: always hashed
     for (uint32_t c_ = cand; c_; c_ &= c_ - 1) {
         int p = __ffs(c_) - 1;
         int cell = r * N + p;
-        uint64_t h2 = h ^ zkey<N>(cell, 1 - ycol);
-        if ((capb >> p) & 1u) h2 ^= S.capx[cell];
+        uint64_t h2 = ((sc >> p) & 1u) ? h : h ^ zkey<N>(cell, 1 - ycol);
+        if (((capb | sc) >> p) & 1u) h2 ^= S.capx[cell];
         if (bloom_maybe(bl, h2)) pend |= 1u << p;
         else legal |= 1u << p;
     }
@@ -314,8 +345,8 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         uint64_t h2 = 0ull;
         if (pend) {
             int cell = r * N + p;
-            h2 = h ^ zkey<N>(cell, 1 - ycol);
-            if ((capb >> p) & 1u) h2 ^= S.capx[cell];
+            h2 = ((sc >> p) & 1u) ? h : h ^ zkey<N>(cell, 1 - ycol);
+            if (((capb | sc) >> p) & 1u) h2 ^= S.capx[cell];
             S.u.sk.hit[lane] = h2;
         }
         __syncwarp();
@@ -564,6 +595,21 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
                 }
                 for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zkey<N>(lane * N + __ffs(d_) - 1, 1 - role);
                 O &= ~dead;
+                if (p.self_capture && !__any_sync(BBK_FULL, dead != 0u)) {
+                    // go.py:249-255: the placed stone's group without a liberty is removed
+                    uint32_t F = lane == ra ? (1u << ca) : 0u;
+                    while (true) {
+                        const uint32_t F2 = (F | dilate<N>(F, lane)) & M;
+                        const bool ch = __any_sync(BBK_FULL, F2 != F);
+                        F = F2;
+                        if (!ch) break;
+                    }
+                    const uint32_t E1 = ~(M | O) & rowm;
+                    if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E1) != 0u)) {
+                        for (uint32_t f_ = F; f_; f_ &= f_ - 1) capxor ^= zkey<N>(lane * N + __ffs(f_) - 1, role);
+                        M &= ~F;
+                    }
+                }
                 const uint64_t h2 = h ^ zkey<N>(a, role) ^ warp_xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
                 const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
@@ -601,7 +647,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
             const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
-            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, lane);
+            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, p.self_capture != 0, lane);
         }
         __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit
@@ -797,7 +843,7 @@ int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const 
     return go::dispatch_step(size, p, (cudaStream_t)stream);
 }
 
-int bbk_go_step(int size, double komi, const bbk_cols* in, const bbk_go_state* in_s,
+int bbk_go_step(int size, double komi, int allow_self_capture, const bbk_cols* in, const bbk_go_state* in_s,
                 const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
                 const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state,
                 const uint64_t* slot_keys, int32_t max_steps, void* stream) {
@@ -805,7 +851,7 @@ int bbk_go_step(int size, double komi, const bbk_cols* in, const bbk_go_state* i
     go::StepParams p{};
     p.in = *in; p.in_s = *in_s; p.out = *out; p.out_s = *out_s; p.store = *store;
     p.actions = actions; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
-    p.max_steps = max_steps; p.komi = komi; p.force_reset = 0;
+    p.max_steps = max_steps; p.komi = komi; p.force_reset = 0; p.self_capture = allow_self_capture;
     return go::dispatch_step(size, p, (cudaStream_t)stream);
 }
 

@@ -72,11 +72,12 @@ class GoStore:
 
 
 class GoKernel(DeviceKernel):
-    def __init__(self, size: int, komi: float = 6.5):
+    def __init__(self, size: int, komi: float = 6.5, allow_self_capture: bool = False):
         if size not in (9, 13, 19):
             raise UnsupportedGame(f"go size {size} has no device kernel (9, 13, 19 are instantiated)")
         self.size = size
         self.komi = float(komi)
+        self.allow_self_capture = bool(allow_self_capture)
         self.cells = size * size
         self.num_actions = self.cells + 1
         self.obs_shape = (size, size, 2 * HISTORY_PLANES + 1)
@@ -133,7 +134,7 @@ class GoKernel(DeviceKernel):
         store.lineage.advance(v.uid, out.uid)
 
     def launch_step(self, v, out, a, ks, sk, limit) -> None:
-        nat.check(nat.lib().bbk_go_step(self.size, self.komi, self.cols(v), self.state_struct(v), self.out_cols(out),
+        nat.check(nat.lib().bbk_go_step(self.size, self.komi, int(self.allow_self_capture), self.cols(v), self.state_struct(v), self.out_cols(out),
                                         self.state_struct(out), out.store.struct(), nat.ptr(a), v.n, v.slot0, ks,
                                         nat.ptr(sk), limit, nat.stream_handle(v.device)), "bbk_go_step")
 
@@ -190,13 +191,11 @@ class GoKernel(DeviceKernel):
 
 def make_game(size: int = 9, komi: float = 6.5, allow_self_capture: bool = False) -> GameDef:
     """Device twin of reference go.make_game (go.py:114-290)."""
-    if allow_self_capture:
-        raise UnsupportedGame("allow_self_capture=True has no device kernel (reference default is False)")
     cells = size * size
     return GameDef(
         spec=GameSpec(f"go_{size}x{size}", 2, (size, size, 2 * HISTORY_PLANES + 1), cells + 1),
         max_steps=512,
-        batch_kernel=GoKernel(size, komi),
+        batch_kernel=GoKernel(size, komi, allow_self_capture),
     )
 
 

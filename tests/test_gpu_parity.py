@@ -39,9 +39,15 @@ def compare(batch, ob, t, check_obs=True, check_encode=True):
                 raise AssertionError(f"step {t}: slot {i} encode differs")
 
 
-def run_pair(oracle, game, n, steps, seed=0, max_steps=None, obs_every=1, enc_every=1):
-    sess = bb.BatchSession(game, n, seed, max_steps=max_steps)
-    orc = oracle.Session(game, n, seed, max_steps=max_steps)
+def _self_capture_game(game):
+    from paper_2303_17503_b200.games import go
+
+    return go.make_game(int(game.split("_")[1].split("x")[0]), allow_self_capture=True)
+
+
+def run_pair(oracle, game, n, steps, seed=0, max_steps=None, obs_every=1, enc_every=1, self_capture=False):
+    sess = bb.BatchSession(_self_capture_game(game) if self_capture else game, n, seed, max_steps=max_steps)
+    orc = oracle.Session(game, n, seed, max_steps=max_steps, self_capture=self_capture)
     compare(sess.batch, orc.b, 0)
     for t in range(1, steps + 1):
         a_dev = sess.sample_random_actions().cpu().numpy()
@@ -69,11 +75,18 @@ def test_device_matches_oracle(oracle, game, n, steps, max_steps):
     run_pair(oracle, game, n, steps, seed=3, max_steps=max_steps)
 
 
+@pytest.mark.parametrize("game,n,steps,max_steps", [("go_9x9", 64, 400, None), ("go_19x19", 16, 250, None),
+                                                   ("go_9x9", 32, 150, 25)])
+def test_self_capture_variant_matches_oracle(oracle, game, n, steps, max_steps):
+    """make_game(allow_self_capture=True) (go.py:155-173, 249-255): suicides legal unless superko."""
+    run_pair(oracle, game, n, steps, seed=11, max_steps=max_steps, self_capture=True, enc_every=5)
+
+
 @pytest.mark.parametrize("name", [n for n in goldens.names() if "config1" not in n])
 def test_device_matches_reference_golden(name):
     rec = goldens.load(name)
     game, n, seed, max_steps = goldens.game_args(rec)
-    sess = bb.BatchSession(game, n, seed, max_steps=max_steps)
+    sess = bb.BatchSession(_self_capture_game(game) if rec.get("self_capture") else game, n, seed, max_steps=max_steps)
     if rec.get("init_fp"):
         assert bb.batch_fingerprint(sess.batch).hex() == rec["init_fp"]
     for t in range(rec["steps"]):

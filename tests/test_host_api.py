@@ -47,12 +47,15 @@ def test_empty_batch_rejected_before_any_device_work():
         bb.batch_init("go_9x9", bb.RngKey(0), 0)
 
 
-def test_self_capture_variant_is_explicitly_unsupported():
+def test_self_capture_variant_and_other_sizes():
     from paper_2303_17503_b200.games import go
 
-    with pytest.raises(bb.UnsupportedGame):
-        go.make_game(9, allow_self_capture=True)
+    g = go.make_game(9, allow_self_capture=True)
+    assert g.batch_kernel.allow_self_capture and g.spec.game_id == "go_9x9"
+    assert not go.GAME.batch_kernel.allow_self_capture
     assert go.make_game(13).spec.num_actions == 170
+    with pytest.raises(bb.UnsupportedGame):
+        go.make_game(11)
 
 
 def test_lineage_allows_head_and_recent_branches():

@@ -16,7 +16,7 @@ FAST = [n for n in goldens.names() if "config1" not in n and not n.startswith("s
 
 def _replay(oracle, rec, check_obs=True, check_slots=True):
     game, n, seed, max_steps = goldens.game_args(rec)
-    sess = oracle.Session(game, n, seed, max_steps=max_steps)
+    sess = oracle.Session(game, n, seed, max_steps=max_steps, self_capture=bool(rec.get("self_capture")))
     if rec.get("init_fp"):
         assert sess.b.batch_fingerprint().hex() == rec["init_fp"]
     for t in range(rec["steps"]):

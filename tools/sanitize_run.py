@@ -1,3 +1,5 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 """Small fused-loop run of every game, for compute-sanitizer (memcheck / racecheck / synccheck)."""
 import sys
 
