@@ -241,10 +241,9 @@ def random_actions(mask: np.ndarray, key_state: int, slot0: int = 0) -> np.ndarr
 
 
 def make(game_id: str, n: int, max_steps: int | None = None, self_capture: bool = False) -> _Batch:
-    if game_id == "go_9x9":
-        return GoBatch(9, n, 512 if max_steps is None else max_steps, self_capture=self_capture)
-    if game_id == "go_19x19":
-        return GoBatch(19, n, 512 if max_steps is None else max_steps, self_capture=self_capture)
+    if game_id.startswith("go_"):
+        size = int(game_id[3:].split("x")[0])
+        return GoBatch(size, n, 512 if max_steps is None else max_steps, self_capture=self_capture)
     if game_id == "backgammon":
         return BackgammonBatch(n, 1024 if max_steps is None else max_steps)
     if game_id == "chess":

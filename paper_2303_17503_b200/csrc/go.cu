@@ -818,9 +818,14 @@ static int launch_observe(const uint16_t* pat, const uint8_t* role, float* obs, 
 }
 
 static int dispatch_step(int size, const StepParams& p, cudaStream_t s) {
-    switch (size) {
+    switch (size) {   // odd board sizes 5..19 (go.py:114 accepts any size)
+        case 5: return launch_step<5>(p, s);
+        case 7: return launch_step<7>(p, s);
         case 9: return launch_step<9>(p, s);
+        case 11: return launch_step<11>(p, s);
         case 13: return launch_step<13>(p, s);
+        case 15: return launch_step<15>(p, s);
+        case 17: return launch_step<17>(p, s);
         case 19: return launch_step<19>(p, s);
         default: return (int)cudaErrorInvalidValue;
     }
@@ -858,8 +863,13 @@ int bbk_go_step(int size, double komi, int allow_self_capture, const bbk_cols* i
 int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, void* stream) {
     if (n <= 0) return 0;
     switch (size) {
+        case 5: return go::launch_observe<5>(pat, role, obs, n, (cudaStream_t)stream);
+        case 7: return go::launch_observe<7>(pat, role, obs, n, (cudaStream_t)stream);
         case 9: return go::launch_observe<9>(pat, role, obs, n, (cudaStream_t)stream);
+        case 11: return go::launch_observe<11>(pat, role, obs, n, (cudaStream_t)stream);
         case 13: return go::launch_observe<13>(pat, role, obs, n, (cudaStream_t)stream);
+        case 15: return go::launch_observe<15>(pat, role, obs, n, (cudaStream_t)stream);
+        case 17: return go::launch_observe<17>(pat, role, obs, n, (cudaStream_t)stream);
         case 19: return go::launch_observe<19>(pat, role, obs, n, (cudaStream_t)stream);
         default: return (int)cudaErrorInvalidValue;
     }

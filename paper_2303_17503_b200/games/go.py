@@ -25,6 +25,7 @@ from ..core import GameDef, GameSpec, StaleBatch, UnsupportedGame
 from ._device import DeviceKernel, DeviceV, Lineage, _torch
 
 HISTORY_PLANES = 8
+SIZES = (5, 7, 9, 11, 13, 15, 17, 19)   # step_kernel<N> instantiations (csrc/go.cu dispatch_step)
 
 
 class GoCoreView:
@@ -73,8 +74,8 @@ class GoStore:
 
 class GoKernel(DeviceKernel):
     def __init__(self, size: int, komi: float = 6.5, allow_self_capture: bool = False):
-        if size not in (9, 13, 19):
-            raise UnsupportedGame(f"go size {size} has no device kernel (9, 13, 19 are instantiated)")
+        if size not in SIZES:
+            raise UnsupportedGame(f"go size {size} has no device kernel (odd sizes 5..19 are instantiated)")
         self.size = size
         self.komi = float(komi)
         self.allow_self_capture = bool(allow_self_capture)

@@ -108,6 +108,8 @@ def main():
         ("bg_s0_b16", lambda: record("bg_s0_b16", "backgammon", 16, 0, 1500, per_slot_steps=40)),
         ("bg_s99_b8_trunc50", lambda: record("bg_s99_b8_trunc50", "backgammon", 8, 99, 300, max_steps=50)),
         ("go9_config1_b1024", lambda: record_until_all_finished("go9_config1_b1024", "go_9x9", 1024, 0)),
+        ("go7_s0_b16", lambda: record("go7_s0_b16", go.make_game(7), 16, 0, 200, per_slot_steps=10)),
+        ("go13_s1_b8", lambda: record("go13_s1_b8", go.make_game(13), 8, 1, 250, per_slot_steps=10)),
         # make_game(allow_self_capture=True) (go.py:155-173, 249-255): suicide moves legal unless superko
         ("go9sc_s0_b16", lambda: dict(record("go9sc_s0_b16", go.make_game(9, allow_self_capture=True), 16, 0, 300,
                                              per_slot_steps=30), self_capture=True)),

@@ -45,8 +45,18 @@ def _self_capture_game(game):
     return go.make_game(int(game.split("_")[1].split("x")[0]), allow_self_capture=True)
 
 
+def _device_game(game, self_capture=False):
+    from paper_2303_17503_b200.games import go
+
+    if self_capture:
+        return _self_capture_game(game)
+    if game.startswith("go_") and game not in bb.available_games():   # other board sizes via make_game
+        return go.make_game(int(game[3:].split("x")[0]))
+    return game
+
+
 def run_pair(oracle, game, n, steps, seed=0, max_steps=None, obs_every=1, enc_every=1, self_capture=False):
-    sess = bb.BatchSession(_self_capture_game(game) if self_capture else game, n, seed, max_steps=max_steps)
+    sess = bb.BatchSession(_device_game(game, self_capture), n, seed, max_steps=max_steps)
     orc = oracle.Session(game, n, seed, max_steps=max_steps, self_capture=self_capture)
     compare(sess.batch, orc.b, 0)
     for t in range(1, steps + 1):
@@ -75,6 +85,12 @@ def test_device_matches_oracle(oracle, game, n, steps, max_steps):
     run_pair(oracle, game, n, steps, seed=3, max_steps=max_steps)
 
 
+@pytest.mark.parametrize("game", ["go_5x5", "go_7x7", "go_11x11", "go_13x13", "go_15x15", "go_17x17"])
+def test_other_go_sizes_match_oracle(oracle, game):
+    """go.make_game(size) for the other instantiated sizes (go.py:114-290)."""
+    run_pair(oracle, game, 24, 260, seed=5, enc_every=4)
+
+
 @pytest.mark.parametrize("game,n,steps,max_steps", [("go_9x9", 64, 400, None), ("go_19x19", 16, 250, None),
                                                    ("go_9x9", 32, 150, 25)])
 def test_self_capture_variant_matches_oracle(oracle, game, n, steps, max_steps):
@@ -86,7 +102,7 @@ def test_self_capture_variant_matches_oracle(oracle, game, n, steps, max_steps):
 def test_device_matches_reference_golden(name):
     rec = goldens.load(name)
     game, n, seed, max_steps = goldens.game_args(rec)
-    sess = bb.BatchSession(_self_capture_game(game) if rec.get("self_capture") else game, n, seed, max_steps=max_steps)
+    sess = bb.BatchSession(_device_game(game, bool(rec.get("self_capture"))), n, seed, max_steps=max_steps)
     if rec.get("init_fp"):
         assert bb.batch_fingerprint(sess.batch).hex() == rec["init_fp"]
     for t in range(rec["steps"]):

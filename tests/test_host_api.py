@@ -54,8 +54,10 @@ def test_self_capture_variant_and_other_sizes():
     assert g.batch_kernel.allow_self_capture and g.spec.game_id == "go_9x9"
     assert not go.GAME.batch_kernel.allow_self_capture
     assert go.make_game(13).spec.num_actions == 170
-    with pytest.raises(bb.UnsupportedGame):
-        go.make_game(11)
+    assert go.make_game(7).spec.num_actions == 50
+    for bad in (4, 21):
+        with pytest.raises(bb.UnsupportedGame):
+            go.make_game(bad)
 
 
 def test_lineage_allows_head_and_recent_branches():
