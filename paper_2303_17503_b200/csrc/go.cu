@@ -443,8 +443,11 @@ __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
     __syncthreads();
 }
 
+// resident CTAs per SM the register budget is sized for: small boards fit 8 (shared memory allows it)
+__host__ __device__ constexpr int min_ctas(int N) { return N <= 13 ? 8 : 6; }
+
 template <int N>
-__global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(StepParams p) {
+__global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepParams p) {
     constexpr int C = N * N;
     constexpr int A = C + 1;
     constexpr int PS = pat_stride(N);
