@@ -315,7 +315,7 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
     asm volatile("cp.async.commit_group;");
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
+__global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 64 registers: 8 CTAs per SM
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
