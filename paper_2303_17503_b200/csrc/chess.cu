@@ -37,7 +37,7 @@ __device__ __constant__ int8_t DIR_DR[8] = {1, 1, 0, -1, -1, -1, 0, 1};
 __device__ __constant__ int8_t DIR_DF[8] = {0, 1, 1, 1, 0, -1, -1, -1};
 
 struct WarpSmem {
-    alignas(16) uint8_t mask[A + 16];
+    alignas(16) uint32_t mbits[A / 32];   // legal mask staged as bits (action a = bit a)
     alignas(16) uint32_t bits[NF / 32 + 4];
     alignas(16) uint8_t bd[64];
     alignas(16) uint8_t packed[32];
@@ -45,7 +45,7 @@ struct WarpSmem {
     uint8_t prep[8];
     uint64_t pinray[8];
     int8_t pinsq[8];
-    uint16_t task[2][136];             // (piece, ray) work units: own [0], opponent [1]
+    uint16_t task[2][96];              // (piece, ray) work units: own [0], opponent [1] (<= 9Q 2R 2B 2N K = 91)
     // next-board prefetch (cp.async): board, packed past boards t = 1..7, ring meta by ply
     alignas(16) uint8_t pf_bd[64];
     alignas(16) uint8_t pf_past[7][32];
@@ -136,13 +136,15 @@ __device__ __forceinline__ int action_of(int fl, int from, int to, int promo) {
 __device__ __constant__ int8_t FLIPD[8] = {4, 3, 2, 1, 0, 7, 6, 5};   // vertical flip of a queen direction
 __device__ __constant__ int8_t FLIPK[8] = {3, 2, 1, 0, 7, 6, 5, 4};   // vertical flip of a knight jump
 
+__device__ __forceinline__ void setm(uint32_t* m, int a) { atomicOr(&m[a >> 5], 1u << (a & 31)); }
+
 __device__ __forceinline__ int ntasks_of(uint8_t pc) {
     const int t = pc & 7;
     return !pc ? 0 : t == Q ? 8 : (t == R || t == B) ? 4 : 1;
 }
 
 // Build both task lists (own = `side`, opponent) with one packed warp scan.
-__device__ void build_tasks(const uint8_t* bd, int side, uint16_t (*task)[136], int& n_own, int& n_opp, int lane) {
+__device__ void build_tasks(const uint8_t* bd, int side, uint16_t (*task)[96], int& n_own, int& n_opp, int lane) {
     const uint8_t p0 = bd[lane], p1 = bd[lane + 32];
     const int o0 = (p0 && color(p0) == side) ? ntasks_of(p0) : 0, o1 = (p1 && color(p1) == side) ? ntasks_of(p1) : 0;
     const int x0 = (p0 && color(p0) != side) ? ntasks_of(p0) : 0, x1 = (p1 && color(p1) != side) ? ntasks_of(p1) : 0;
@@ -196,7 +198,7 @@ __device__ __forceinline__ uint64_t task_attacks(const uint8_t* bd, uint16_t tk,
 
 struct GenCtx {
     const uint8_t* bd;
-    uint8_t* mask;
+    uint32_t* mask;   // bit per action
     int side, fl, ksq, ep;
     uint64_t att, checkmask;
     const int8_t* pinsq;
@@ -217,7 +219,7 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
             const int to = rr * 8 + ff;
             const uint8_t q = c.bd[to];
             if ((q && color(q) == side) || ((c.att >> to) & 1ull)) continue;
-            c.mask[from + (c.fl ? FLIPD[k] : k) * 7] = 1; cnt++;
+            setm(c.mask, from + (c.fl ? FLIPD[k] : k) * 7); cnt++;
         }
         return cnt;
     }
@@ -231,7 +233,7 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
             const int to = rr * 8 + ff;
             const uint8_t q = c.bd[to];
             if (q && color(q) == side) break;
-            if ((allow >> to) & 1ull) { c.mask[from + dm + k] = 1; cnt++; }
+            if ((allow >> to) & 1ull) { setm(c.mask, from + dm + k); cnt++; }
             if (q) break;
             rr += DIR_DR[d]; ff += DIR_DF[d]; k++;
         }
@@ -244,7 +246,7 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
             const int to = rr * 8 + ff;
             const uint8_t q = c.bd[to];
             if ((q && color(q) == side) || !((allow >> to) & 1ull)) continue;
-            c.mask[from + 56 + (c.fl ? FLIPK[k] : k)] = 1; cnt++;
+            setm(c.mask, from + 56 + (c.fl ? FLIPK[k] : k)); cnt++;
         }
         return cnt;
     }
@@ -253,13 +255,13 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
     const int r1 = r + dr;
     auto emit = [&](int to, int df, int plane_q) {
         if (r1 == last) {
-            c.mask[from + plane_q] = 1;                       // queen promotion = queen-move plane
-            c.mask[from + 64 + 0 * 3 + df + 1] = 1;           // N, B, R under-promotions
-            c.mask[from + 64 + 1 * 3 + df + 1] = 1;
-            c.mask[from + 64 + 2 * 3 + df + 1] = 1;
+            setm(c.mask, from + plane_q);                       // queen promotion = queen-move plane
+            setm(c.mask, from + 64 + 0 * 3 + df + 1);           // N, B, R under-promotions
+            setm(c.mask, from + 64 + 1 * 3 + df + 1);
+            setm(c.mask, from + 64 + 2 * 3 + df + 1);
             cnt += 4;
         } else {
-            c.mask[from + plane_q] = 1; cnt++;
+            setm(c.mask, from + plane_q); cnt++;
         }
     };
     const int to1 = r1 * 8 + f;
@@ -278,7 +280,7 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
         } else if (to == c.ep) {
             const int cap = side == 0 ? to - 8 : to + 8;
             if (!attacked_mod(c.bd, c.ksq, 1 - side, sq, cap, to, pc)) {
-                c.mask[from + plane] = 1; cnt++;
+                setm(c.mask, from + plane); cnt++;
                 ep_legal = true;
             }
         }
@@ -365,7 +367,7 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
     asm volatile("cp.async.commit_group;");
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
+__global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 56 registers, no spills
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
@@ -436,7 +438,8 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             ep = __shfl_sync(BBK_FULL, ep, 0); halfmove = __shfl_sync(BBK_FULL, halfmove, 0);
         }
         // zero the mask staging area while the board settles
-        for (int i = lane; i < A / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = lane; i < A / 128; i += 32) reinterpret_cast<uint4*>(S.mbits)[i] = make_uint4(0, 0, 0, 0);
+        if (lane < (A / 32) % 4) S.mbits[A / 32 - 1 - lane] = 0u;
         __syncwarp();
         const int side = stm, opp = 1 - side, fl = side ? 56 : 0;
         // ---- king, attack map, checks, pins
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         const uint64_t blockall = warp_or64(block);
         __syncwarp();
         GenCtx c;
-        c.bd = S.bd; c.mask = S.mask; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
+        c.bd = S.bd; c.mask = S.mbits; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
         c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
         c.pinsq = S.pinsq; c.pinray = S.pinray;
         bool ep_legal = false;
@@ -501,11 +504,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             if (ksq == rank + 4) {
                 if ((castle & kbit) && S.bd[rank + 7] == mk(side, R) && !S.bd[rank + 5] && !S.bd[rank + 6] &&
                     !((att >> (rank + 5)) & 1ull) && !((att >> (rank + 6)) & 1ull)) {
-                    S.mask[action_of(fl, ksq, rank + 6, 0)] = 1; cnt++;
+                    setm(S.mbits, action_of(fl, ksq, rank + 6, 0)); cnt++;
                 }
                 if ((castle & qbit) && S.bd[rank + 0] == mk(side, R) && !S.bd[rank + 1] && !S.bd[rank + 2] &&
                     !S.bd[rank + 3] && !((att >> (rank + 3)) & 1ull) && !((att >> (rank + 2)) & 1ull)) {
-                    S.mask[action_of(fl, ksq, rank + 2, 0)] = 1; cnt++;
+                    setm(S.mbits, action_of(fl, ksq, rank + 2, 0)); cnt++;
                 }
             }
         }
@@ -562,7 +565,8 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
         const bool truncated = !terminal && step >= p.max_steps;
         eps += (terminal || truncated) ? 1 : 0;
         if (p.out.next_actions) {   // fused agents.random_actions on the new mask (still in shared memory)
-            const int64_t a = warp_sample_bytes(S.mask, A, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
+            __syncwarp();
+            const int64_t a = warp_sample_bits(S.mbits, A / 32, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
                                                 p.slot0 + b);
             if (lane == 0) p.out.next_actions[b] = a;
         }
@@ -643,12 +647,13 @@ __global__ void __launch_bounds__(kWarps * 32, 6) step_kernel(Params p) {
             orec[119 * (lane + 32) + 118] = cnt118;
         }
         // ---- mask: zero when finished, else the staged bytes
-        if (terminal || truncated) {
-            for (int i = lane; i < A / 16; i += 32) reinterpret_cast<uint4*>(S.mask)[i] = make_uint4(0, 0, 0, 0);
-            __syncwarp();
-        }
+        // mask bytes from the staged bits: 16 actions per 16-byte store, zero when finished
         uint4* m4 = reinterpret_cast<uint4*>(p.out.legal_action_mask + b * (int64_t)A);
-        for (int i = lane; i < A / 16; i += 32) m4[i] = reinterpret_cast<const uint4*>(S.mask)[i];
+        const bool live = !(terminal || truncated);
+        for (int i = lane; i < A / 16; i += 32) {
+            const uint32_t v = live ? (S.mbits[i >> 1] >> (16 * (i & 1))) & 0xFFFFu : 0u;
+            m4[i] = make_uint4(spread4(v & 15u), spread4((v >> 4) & 15u), spread4((v >> 8) & 15u), spread4(v >> 12));
+        }
         uint8_t* ob = p.out_s.board + b * 64;
         ob[lane] = S.bd[lane]; ob[lane + 32] = S.bd[lane + 32];
         if (lane == 0) {

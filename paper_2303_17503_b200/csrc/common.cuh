@@ -103,6 +103,46 @@ __device__ __forceinline__ uint32_t chunk_count_bytes(uint4 v) {
     return __popc(v.x & 0x01010101u) + __popc(v.y & 0x01010101u) + __popc(v.z & 0x01010101u) +
            __popc(v.w & 0x01010101u);
 }
+// 4 bits -> 4 bytes of 0 / 1 (bit k -> byte k)
+__device__ __forceinline__ uint32_t spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+// agents.random_actions for ONE slot whose legal mask is staged as bits (action a = bit a of
+// bits[a / 32], nwords words): lanes count contiguous word ranges, scan, and the lane holding
+// the d-th set bit resolves it; d = child(key, slot) % count, 0 when count == 0.
+__device__ __forceinline__ int64_t warp_sample_bits(const uint32_t* bits, int nwords, int count, uint64_t key,
+                                                    int64_t slot) {
+    if (count <= 0) return 0;
+    const int lane = lane_id();
+    const int d = (int)(child(key, (uint64_t)slot) % (uint64_t)count);
+    const int per = (nwords + 31) >> 5;
+    const int w0 = lane * per, w1 = min(w0 + per, nwords);
+    int c = 0;
+    for (int i = w0; i < w1; i++) c += __popc(bits[i]);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(BBK_FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int excl = incl - c;
+    int64_t act = -1;
+    if (d >= excl && d < incl) {
+        int r = d - excl;
+        for (int i = w0; i < w1; i++) {
+            uint32_t v = bits[i];
+            const int pc = __popc(v);
+            if (r < pc) {
+                for (; r > 0; r--) v &= v - 1;
+                act = 32 * i + __ffs(v) - 1;
+                break;
+            }
+            r -= pc;
+        }
+    }
+    const unsigned who = __ballot_sync(BBK_FULL, act >= 0);
+    return __shfl_sync(BBK_FULL, act, __ffs(who) - 1);
+}
+
 __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A, int count, uint64_t key,
                                                      int64_t slot) {
     if (count <= 0) return 0;
