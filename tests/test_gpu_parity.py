@@ -138,7 +138,10 @@ def test_large_batch_vs_oracle_columns(oracle, game):
     run_pair(oracle, game, n, steps, seed=11, obs_every=10, enc_every=30)
 
 
-@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"])
+SMALL = ["tic_tac_toe", "connect_four", "othello", "hex", "2048", "kuhn_poker", "leduc_holdem"]
+
+
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"] + SMALL)
 def test_batch_step_equals_scalar_steps(game):
     """Port of reference test_core.py:179-196 on the device scalar API."""
     root = bb.RngKey(71)
@@ -184,30 +187,32 @@ def test_branching_previous_batch_steps_identically():
     assert bb.batch_fingerprint(b1) == bb.batch_fingerprint(bb.batch_step(b0, acts, root.child(2)))
 
 
-def test_slot_sharding_is_bit_identical():
+@pytest.mark.parametrize("game", ["go_19x19", "backgammon", "chess", "shogi", "hex", "2048", "leduc_holdem"])
+def test_slot_sharding_is_bit_identical(game):
     """Slot ranges run with slot0 offsets (one per GPU rank) equal the full batch's rows."""
     import torch
     from paper_2303_17503_b200.core import resolve
 
-    gdef = resolve("go_19x19")
+    gdef = resolve(game)
     kern = gdef.batch_kernel
     n, parts = 64, 4
+    lim = gdef.max_steps
     root = bb.RngKey(9)
-    full = kern.init(gdef, root.child(0), n, 512)
-    shards = [kern.init(gdef, root.child(0), n // parts, 512, slot0=r * (n // parts)) for r in range(parts)]
+    full = kern.init(gdef, root.child(0), n, lim)
+    shards = [kern.init(gdef, root.child(0), n // parts, lim, slot0=r * (n // parts)) for r in range(parts)]
     for t in range(1, 40):
         a = kern.random_actions(full, root.child(2 * t - 1))
-        full = kern.step(gdef, full, a, root.child(2 * t), 512, validate=False)
+        full = kern.step(gdef, full, a, root.child(2 * t), lim, validate=False)
         for r in range(parts):
             sa = kern.random_actions(shards[r], root.child(2 * t - 1))
             assert torch.equal(sa, a[r * 16:(r + 1) * 16])
-            shards[r] = kern.step(gdef, shards[r], sa, root.child(2 * t), 512, validate=False)
+            shards[r] = kern.step(gdef, shards[r], sa, root.child(2 * t), lim, validate=False)
     for r in range(parts):
-        for name in ("observation", "legal_action_mask", "rewards", "current_player"):
+        for name in ("observation", "legal_action_mask", "rewards", "current_player", "step_count"):
             assert torch.equal(getattr(shards[r].dev, name), getattr(full.dev, name)[r * 16:(r + 1) * 16]), name
 
 
-@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"])
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi"] + SMALL)
 def test_fused_sampling_and_episode_counter(game):
     """Step kernels that also sample the next random actions equal the separate sampler kernel."""
     import torch
