@@ -140,6 +140,12 @@ def ptr(t) -> int | None:
 
 
 def stream_handle(device=None) -> int:
+    """cudaStream_t of torch's current stream on `device`, made the CUDA runtime's current device too:
+    every launch goes through here, and a kernel must run on the device that owns its buffers."""
     import torch
 
+    if device is not None:
+        idx = device.index if isinstance(device, torch.device) else int(device)
+        if idx is not None and torch.cuda.current_device() != idx:
+            torch.cuda.set_device(idx)
     return torch.cuda.current_stream(device).cuda_stream
