@@ -210,7 +210,11 @@ class DeviceKernel:
         if isinstance(actions, torch.Tensor):
             a = actions
             if a.device != v.device or a.dtype != torch.int64:
-                a = a.to(device=v.device, dtype=torch.int64)
+                # a pinned host int64 buffer is copied asynchronously on the launch stream (the step
+                # kernel is ordered after it; the caller must not rewrite the buffer before the
+                # step's results are read, as with any CUDA async copy)
+                pinned = a.device.type == "cpu" and a.dtype == torch.int64 and a.is_pinned()
+                a = a.to(device=v.device, dtype=torch.int64, non_blocking=pinned)
         else:
             arr = np.ascontiguousarray(np.asarray(actions, dtype=np.int64))
             a = torch.from_numpy(arr).to(v.device)
