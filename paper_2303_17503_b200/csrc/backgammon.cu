@@ -45,41 +45,77 @@ struct Board {
 
 __device__ __constant__ int8_t kStart[24] = {2, 0, 0, 0, 0, -5, 0, -3, 0, 0, 0, 5, -5, 0, 0, 0, 3, 0, 5, 0, 0, 0, 0, -2};
 
-// _legal_mask (backgammon.py:62-95) as 5 words of action bits.
-__device__ void legal_mask(const Board& s, uint32_t m[5]) {
+// Board points are read and written with run-time indices through these unrolled
+// compare-and-select loops, so `pts` stays in registers (a dynamically indexed local array
+// would live in local memory: every access a long-scoreboard round trip).
+__device__ __forceinline__ int get_pt(const Board& s, int a) {
+    int v = 0;
+#pragma unroll
+    for (int j = 0; j < 24; j++) v = j == a ? (int)s.pts[j] : v;
+    return v;
+}
+__device__ __forceinline__ void add_pt(Board& s, int a, int d) {
+#pragma unroll
+    for (int j = 0; j < 24; j++) s.pts[j] = (int8_t)(j == a ? s.pts[j] + d : s.pts[j]);
+}
+__device__ __forceinline__ void set_pt(Board& s, int a, int v) {
+#pragma unroll
+    for (int j = 0; j < 24; j++) s.pts[j] = (int8_t)(j == a ? v : s.pts[j]);
+}
+// bar / off of a run-time role, by select (a role-indexed array would live in local memory)
+__device__ __forceinline__ int bar_of(const Board& s, int r) { return r ? s.bar[1] : s.bar[0]; }
+__device__ __forceinline__ int off_of(const Board& s, int r) { return r ? s.off[1] : s.off[0]; }
+__device__ __forceinline__ void add_bar(Board& s, int r, int d) { if (r) s.bar[1] += d; else s.bar[0] += d; }
+__device__ __forceinline__ void add_off(Board& s, int r, int d) { if (r) s.off[1] += d; else s.off[0] += d; }
+
+// OR action bit `bit` into the 5 mask words (held in registers)
+__device__ __forceinline__ void set_bit5(uint32_t m[5], int bit) {
+    const int w = bit >> 5;
+    const uint32_t v = 1u << (bit & 31);
+#pragma unroll
+    for (int j = 0; j < 5; j++) m[j] |= j == w ? v : 0u;
+}
+
+// _legal_mask (backgammon.py:62-95) as 5 words of action bits, bit-parallel over pips:
+// OWN / BLOCK (>= 2 opponent checkers) as 24-bit pip masks (bit p-1 = pip p, mover frame), then
+// per die the movable pips are OWN & ~(BLOCK << die) above the die, plus bear-offs.
+__device__ __forceinline__ void legal_mask(const Board& s, uint32_t m[5]) {
 #pragma unroll
     for (int j = 0; j < 5; j++) m[j] = 0u;
     const int role = s.role, sign = role == 0 ? 1 : -1;
     uint32_t dset = 0u;
-    for (int j = 0; j < s.nrem; j++) dset |= 1u << s.rem[j];
+#pragma unroll
+    for (int j = 0; j < 4; j++) dset |= j < s.nrem ? 1u << s.rem[j] : 0u;
+    uint32_t own = 0u, blk = 0u;   // absolute point order first
+#pragma unroll
+    for (int j = 0; j < 24; j++) {
+        const int v = s.pts[j] * sign;
+        own |= (uint32_t)(v > 0) << j;
+        blk |= (uint32_t)(v <= -2) << j;
+    }
+    if (role == 0) { own = __brev(own) >> 8; blk = __brev(blk) >> 8; }   // pip p <-> point 24 - p
     bool any = false;
-    if (s.bar[role] > 0) {
+    if (bar_of(s, role) > 0) {   // enter on pip 25 - die
         for (int die = 1; die <= 6; die++) {
             if (!((dset >> die) & 1u)) continue;
-            int dest = role == 0 ? die - 1 : 24 - die;
-            if (s.pts[dest] * sign >= -1) { int bit = 6 + die - 1; m[bit >> 5] |= 1u << (bit & 31); any = true; }
+            if (!((blk >> (24 - die)) & 1u)) { set_bit5(m, 6 + die - 1); any = true; }
         }
         if (!any) m[0] |= 1u;
         return;
     }
-    int rear = 0;
-    for (int a = 0; a < 24; a++)
-        if (s.pts[a] * sign > 0) { int pip = role == 0 ? 24 - a : a + 1; rear = pip > rear ? pip : rear; }
+    const int rear = own ? 32 - __clz(own) : 0;   // rearmost own pip
     const bool can_bear_off = rear <= 6;
     for (int die = 1; die <= 6; die++) {
         if (!((dset >> die) & 1u)) continue;
-        for (int pip = 1; pip <= 24; pip++) {
-            int src = role == 0 ? 24 - pip : pip - 1;
-            if (s.pts[src] * sign < 1) continue;
-            int target = pip - die;
-            bool ok;
-            if (target >= 1) {
-                int dest = role == 0 ? 24 - target : target - 1;
-                ok = s.pts[dest] * sign >= -1;
-            } else {
-                ok = can_bear_off && (die == pip || pip == rear);
-            }
-            if (ok) { int bit = (pip + 1) * 6 + die - 1; m[bit >> 5] |= 1u << (bit & 31); any = true; }
+        uint32_t mv = own & ~(blk << die) & ~((1u << die) - 1u);   // pip - die >= 1, target not blocked
+        if (can_bear_off) {                                        // pip - die < 1: die == pip or pip == rear
+            mv |= own & (1u << (die - 1));
+            if (rear >= 1 && rear <= die) mv |= 1u << (rear - 1);
+        }
+        for (; mv; mv &= mv - 1) {
+            const int pip = __ffs(mv);
+            set_bit5(m, (pip + 1) * 6 + die - 1);
+            any = true;
         }
     }
     if (!any) m[0] |= 1u;
@@ -94,18 +130,18 @@ __device__ __forceinline__ void roll(Board& s, int role, uint64_t key) {
     s.terminal = false; s.rr0 = s.rr1 = 0.0f;
 }
 
-__device__ __forceinline__ int sgn_at(const Board& s, int role, int a) { return role == 0 ? s.pts[a] : -s.pts[a]; }
+__device__ __forceinline__ int sgn_at(const Board& s, int role, int a) { const int v = get_pt(s, a); return role == 0 ? v : -v; }
 __device__ __forceinline__ int abs_point(int role, int pip) { return role == 0 ? 24 - pip : pip - 1; }
 
-__device__ void final_(Board& s, int winner) {
+__device__ __forceinline__ void final_(Board& s, int winner) {
     int loser = 1 - winner;
     float value = 1.0f;
-    if (s.off[loser] == 0) {
+    if (off_of(s, loser) == 0) {
         value = 2.0f;
         bool in_home = false;
         int lo = winner == 0 ? 18 : 0;
         for (int a = lo; a < lo + 6; a++) in_home |= sgn_at(s, loser, a) > 0;
-        if (s.bar[loser] > 0 || in_home) value = 3.0f;
+        if (bar_of(s, loser) > 0 || in_home) value = 3.0f;
     }
     s.rr0 = winner == 0 ? value : -value;
     s.rr1 = winner == 0 ? -value : value;
@@ -115,37 +151,50 @@ __device__ void final_(Board& s, int winner) {
 }
 
 // _apply (backgammon.py:150-193)
-__device__ void apply(Board& s, int action, uint64_t key) {
+__device__ __forceinline__ void apply(Board& s, int action, uint64_t key) {
     const int role = s.role;
     const int src = action / 6, die = action - 6 * src + 1;
     if (src == 0) { roll(s, 1 - role, key); return; }
     const int delta = role == 0 ? 1 : -1;
     int target;
-    if (src == 1) { s.bar[role] -= 1; target = 25 - die; }
-    else { int pip = src - 1; s.pts[abs_point(role, pip)] -= (int8_t)delta; target = pip - die; }
+    if (src == 1) { add_bar(s, role, -1); target = 25 - die; }
+    else { int pip = src - 1; add_pt(s, abs_point(role, pip), -delta); target = pip - die; }
     if (src != 1 && target < 1) {
-        s.off[role] += 1;
+        add_off(s, role, 1);
     } else {
         int a = abs_point(role, target);
-        if (sgn_at(s, role, a) == -1) { s.pts[a] = (int8_t)delta; s.bar[1 - role] += 1; }
-        else s.pts[a] += (int8_t)delta;
+        if (sgn_at(s, role, a) == -1) { set_pt(s, a, delta); add_bar(s, 1 - role, 1); }
+        else add_pt(s, a, delta);
     }
-    if (s.off[role] == 15) { final_(s, role); return; }
-    int j = 0;
-    while (j < s.nrem && s.rem[j] != die) j++;
-    for (; j + 1 < s.nrem; j++) s.rem[j] = s.rem[j + 1];
-    if (s.nrem > 0) { s.nrem -= 1; s.rem[s.nrem & 3] = 0; }
+    if (off_of(s, role) == 15) { final_(s, role); return; }
+    // consume the first remaining die equal to `die` (unrolled: rem stays in registers)
+    int idx = 4;
+#pragma unroll
+    for (int j = 0; j < 4; j++) idx = (idx == 4 && j < s.nrem && s.rem[j] == die) ? j : idx;
+#pragma unroll
+    for (int j = 0; j < 3; j++) s.rem[j] = (j >= idx && j + 1 < s.nrem) ? s.rem[j + 1] : s.rem[j];
+    if (s.nrem > 0) {
+        s.nrem -= 1;
+#pragma unroll
+        for (int j = 0; j < 4; j++) s.rem[j] = j == s.nrem ? (uint8_t)0 : s.rem[j];
+    }
     if (s.nrem == 0) { roll(s, 1 - role, key); return; }
     s.rr0 = s.rr1 = 0.0f;
 }
 
-__device__ void observe(const Board& s, int role, float* o /* 34, shared */) {
-    for (int pip = 1; pip <= 24; pip++) o[pip - 1] = (float)sgn_at(s, role, abs_point(role, pip));
-    o[24] = s.bar[role]; o[25] = s.bar[1 - role];
-    o[26] = s.off[role]; o[27] = s.off[1 - role];
-    float cnt[6] = {0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < s.nrem; j++) cnt[s.rem[j] - 1] += 1.0f;
-    for (int d = 0; d < 6; d++) o[28 + d] = cnt[d];
+__device__ __forceinline__ void observe(const Board& s, int role, float* o /* 34, shared */) {
+#pragma unroll
+    for (int pip = 1; pip <= 24; pip++)   // role 0: point 24 - pip, role 1: point pip - 1 (negated)
+        o[pip - 1] = role == 0 ? (float)s.pts[24 - pip] : (float)(-s.pts[pip - 1]);
+    o[24] = bar_of(s, role); o[25] = bar_of(s, 1 - role);
+    o[26] = off_of(s, role); o[27] = off_of(s, 1 - role);
+#pragma unroll
+    for (int d = 0; d < 6; d++) {   // remaining-dice histogram
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) c += (j < s.nrem && s.rem[j] == d + 1) ? 1 : 0;
+        o[28 + d] = (float)c;
+    }
 }
 
 __device__ __forceinline__ void load_board(Board& s, const bbk_bg_state& st, int64_t b) {
@@ -210,6 +259,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
                 int64_t act = 0;
                 if (count > 0) {
                     int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)count);
+#pragma unroll
                     for (int j = 0; j < 5; j++) {
                         const int pc = __popc(m[j]);
                         if (d < pc) {
@@ -235,8 +285,10 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
             p.out.current_player[b] = p2r0 == s.role ? 0 : 1;
             p.out.player_to_role[2 * b] = p2r0; p.out.player_to_role[2 * b + 1] = p2r1;
             // stage mask bytes (record phase = (base*A) & 15, constant per warp)
-            uint8_t* mrow = S.mb + ((base * A) & 15) + lane * A;
-            for (int j = 0; j < A; j++) mrow[j] = (uint8_t)((m[j >> 5] >> (j & 31)) & 1u);
+            // base is a multiple of 32, so the record phase is 0 and rows are 4-byte aligned (A = 4 * 39)
+            uint32_t* mrow = reinterpret_cast<uint32_t*>(S.mb + lane * A);
+#pragma unroll
+            for (int w = 0; w < A / 4; w++) mrow[w] = spread4((m[(4 * w) >> 5] >> ((4 * w) & 31)) & 15u);
             if (p.out.observation) observe(s, s.role, S.ob + ((base * OBS) & 3) + lane * OBS);
         }
         __syncwarp();
