@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
                 const int count = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]) + __popc(m[4]);
                 int64_t act = 0;
                 if (count > 0) {
-                    int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)count);
+                    int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)count);   // (umod_small measured slower here)
 #pragma unroll
                     for (int j = 0; j < 5; j++) {
                         const int pc = __popc(m[j]);

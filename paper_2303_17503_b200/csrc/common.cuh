@@ -24,6 +24,16 @@ __host__ __device__ __forceinline__ uint64_t child(uint64_t s, uint64_t i) {
     return mix64(s + (i + 1) * 0x9E3779B97F4A7C15ULL);
 }
 
+// x mod d for a small divisor (1 <= d < 2^16: action counts, empty cells) with 32-bit
+// arithmetic: x = hi 2^32 + lo, so x mod d = ((hi mod d)(2^32 mod d) + lo mod d) mod d and the
+// sum stays below 2^32. Identical to x % d (the reference's `state % bound`, rng.py:97-101)
+// without the 64-bit division subroutine.
+__device__ __forceinline__ uint32_t umod_small(uint64_t x, uint32_t d) {
+    const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+    const uint32_t r32 = (0u - d) % d;   // 2^32 mod d
+    return ((hi % d) * r32 + lo % d) % d;
+}
+
 __device__ __forceinline__ uint64_t slot_key(const uint64_t* slot_keys, uint64_t key, int64_t slot0, int64_t i) {
     return slot_keys ? slot_keys[i] : child(key, (uint64_t)(slot0 + i));
 }
@@ -113,7 +123,7 @@ __device__ __forceinline__ int64_t warp_sample_bits(const uint32_t* bits, int nw
                                                     int64_t slot) {
     if (count <= 0) return 0;
     const int lane = lane_id();
-    const int d = (int)(child(key, (uint64_t)slot) % (uint64_t)count);
+    const int d = (int)umod_small(child(key, (uint64_t)slot), (uint32_t)count);
     const int per = (nwords + 31) >> 5;
     const int w0 = lane * per, w1 = min(w0 + per, nwords);
     int c = 0;
@@ -147,7 +157,7 @@ __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A,
                                                      int64_t slot) {
     if (count <= 0) return 0;
     const int lane = lane_id();
-    const int d = (int)(child(key, (uint64_t)slot) % (uint64_t)count);
+    const int d = (int)umod_small(child(key, (uint64_t)slot), (uint32_t)count);
     const uintptr_t base = reinterpret_cast<uintptr_t>(mask);
     const int head = (int)(base & 15);
     const uint4* w = reinterpret_cast<const uint4*>(base - head);

@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             const int total = live ? cells + 1 : 0;   // + pass
             int64_t act = 0;
             if (total > 0) {
-                const int d = (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)total);
+                const int d = (int)umod_small(child(p.out.next_key, (uint64_t)(p.slot0 + b)), (uint32_t)total);
                 if (d == cells) act = C;
                 else {
                     const bool mine = d >= incl - c && d < incl;

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
     if (p.out.next_actions) {
         const int cnt = m.count();
         int64_t act = 0;
-        if (cnt > 0) act = select_bit(m, (int)(child(p.out.next_key, (uint64_t)(p.slot0 + b)) % (uint64_t)cnt));
+        if (cnt > 0) act = select_bit(m, (int)umod_small(child(p.out.next_key, (uint64_t)(p.slot0 + b)), (uint32_t)cnt));
         p.out.next_actions[b] = act;
     }
     if (p.out.episodes && (terminal || truncated)) atomicAdd(p.out.episodes, 1ull);

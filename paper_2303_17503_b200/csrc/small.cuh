@@ -346,7 +346,7 @@ struct Play2048 {
     __device__ static void spawn(uint8_t* board, uint64_t key) {   // play2048.py:69-75
         int empties = 0;
         for (int i = 0; i < 16; i++) empties += board[i] == 0;
-        int pick = (int)(child(key, 0) % (uint64_t)empties);
+        int pick = (int)umod_small(child(key, 0), (uint32_t)empties);
         const uint8_t e = (child(key, 1) % 10ull) == 9ull ? 2 : 1;
         for (int i = 0; i < 16; i++)
             if (board[i] == 0 && pick-- == 0) { board[i] = e; break; }

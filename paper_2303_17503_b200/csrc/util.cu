@@ -35,7 +35,7 @@ __global__ void random_actions_kernel(const uint8_t* mask, int64_t n, int A, uin
         int cnt = 0;
         for (int w = lane; w < nwords; w += 32) cnt += __popc(row_word(mask, rs, A, w));
         const int total = warp_sum(cnt);
-        const uint64_t d64 = child(key, (uint64_t)(slot0 + b)) % (uint64_t)(total > 0 ? total : 1);
+        const uint64_t d64 = umod_small(child(key, (uint64_t)(slot0 + b)), (uint32_t)(total > 0 ? total : 1));
         const int d = (int)d64;
         int64_t action = 0;
         if (total > 0) {
