@@ -37,6 +37,15 @@ B_ALG = {"go_9x9": 5964, "go_19x19": 25860, "chess": 35502, "shogi": 41013, "bac
 DEFAULT_BATCH = {"go_9x9": 1 << 17, "go_19x19": 1 << 17, "chess": 1 << 17, "shogi": 1 << 16, "backgammon": 1 << 17}
 STEP_KERNEL = {"go_9x9": "go::step_kernel<9>", "go_19x19": "go::step_kernel<19>", "chess": "chess::step_kernel",
                "shogi": "shogi::step_kernel", "backgammon": "bg::step_kernel"}
+# The reference's small engines: (obs floats, actions, players, Core.encode bytes);
+# B_alg = action 8 + obs + mask + rewards + flags/player/step + player_to_role + encoded Core r/w.
+SMALL = {"tic_tac_toe": (18, 9, 2, 10, "TicTacToe"), "connect_four": (84, 7, 2, 15, "ConnectFour"),
+         "othello": (128, 65, 2, 18, "Othello"), "hex": (484, 122, 2, 35, "Hex"), "2048": (496, 4, 1, 24, "Play2048"),
+         "kuhn_poker": (7, 4, 2, 8, "Kuhn"), "leduc_holdem": (34, 3, 2, 9, "Leduc")}
+for _g, (_o, _a, _p, _e, _k) in SMALL.items():
+    B_ALG[_g] = 8 + 4 * _o + _a + 4 * _p + 10 + _p + 2 * _e
+    DEFAULT_BATCH[_g] = 1 << 17
+    STEP_KERNEL[_g] = f"small::step_kernel<{_k}>"
 METRIC = "random-play env steps/sec"
 
 
@@ -280,7 +289,8 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     batch = Batch(gdef, B, gdef.max_steps, vstate=kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0,
                                                             device=dev, next_key=root.child(1)))
     host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
-    host_r = torch.empty((B, 2), dtype=torch.float32, pin_memory=True)
+    P = gdef.spec.num_players
+    host_r = torch.empty((B, P), dtype=torch.float32, pin_memory=True)
     host_f = torch.empty((B, 2), dtype=torch.uint8, pin_memory=True)
     host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
     t = 0
@@ -318,7 +328,7 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
     return {"value": B * world * args.steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
-            "d2h_bytes_per_step": (8 + 2 + 4 + 8) * B, "steps": args.steps,
+            "d2h_bytes_per_step": (4 * P + 2 + 4 + 8) * B, "steps": args.steps,
             "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player, "
                     "same window as value (fresh init, W warm-up, K timed)"}
 
@@ -382,6 +392,10 @@ def cpu_run(game, n, seconds, threads):
 
 def cpu_baseline(args, game, B, seconds):
     threads = os.cpu_count() or 1
+    if game in SMALL:
+        return {"value": None, "unit": "env-steps/s", "cores": threads, "kind": "port",
+                "sample": "none: oracle/ has no restatement of the small engines (their parity is pinned to "
+                          "reference goldens); see the go/chess/shogi/backgammon lines"}
     n = min(B, 512 if game in ("go_19x19", "chess", "shogi") else 4096)
     v, steps, dt = cpu_run(game, n, seconds, threads)
     return {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "port",
@@ -391,6 +405,8 @@ def cpu_baseline(args, game, B, seconds):
 
 def run_reference(args, rank, world):
     game = args.game
+    if game in SMALL:
+        return {"impl": "reference", "unavailable": f"{game}: no CPU restatement in oracle/ (pinned to reference goldens)"}
     B = args.batch or DEFAULT_BATCH[game]
     threads = os.cpu_count() or 1
     n = min(B, 512 if game in ("go_19x19", "chess", "shogi") else 4096)

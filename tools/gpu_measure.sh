@@ -25,3 +25,10 @@ if [ "${NCU:-1}" = "1" ]; then
     echo "ncu $g rc=$?"
   done
 fi
+# the reference's small engines: device lines only (no CPU oracle)
+if [ "${SMALL:-1}" = "1" ]; then
+  for g in tic_tac_toe connect_four othello hex 2048 kuhn_poker leduc_holdem; do
+    python bench.py --game $g --steps 256 --warmup 8 --no-cpu-baseline --no-sweep > $OUT/bench_$g.json 2> $OUT/bench_$g.err
+    echo "$g rc=$?"
+  done
+fi

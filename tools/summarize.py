@@ -82,6 +82,21 @@ none`; `go19_launches.csv` is the launch list of a short default bench (`--metri
 gpu__time_duration.sum`): the step kernel is the only kernel in the timed loop.
 
 """
+    small = []
+    for g in ("tic_tac_toe", "connect_four", "othello", "hex", "2048", "kuhn_poker", "leduc_holdem"):
+        src = os.path.join(OUT, f"bench_{g}.json")
+        if os.path.exists(src):
+            shutil.copy(src, os.path.join(dst, f"bench_{g}.json"))
+            d = line(src)
+            small.append(f"| {g} | {d['value'] / 1e6:,.1f} M | {d['roofline']['frac']:.3f} | "
+                         f"{d['e2e']['value'] / 1e6:,.1f} M | {d['roofline']['bytes_per_env_step']:,} |")
+    if small:
+        head += """The reference's small engines (SURVEY §8f rank 4; thread per slot, B = 2^17, parity pinned to
+reference goldens, no CPU oracle):
+
+| game | env-steps/s | kernel frac of HBM roofline | e2e | B_alg |
+|---|---|---|---|---|
+""" + "\n".join(small) + "\n\n"
     path = os.path.join(dst, "SUMMARY.md")
     tail = ""
     if os.path.exists(path):
