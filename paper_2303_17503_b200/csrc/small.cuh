@@ -115,12 +115,13 @@ struct ConnectFour {
     }
     __device__ static void observe(const St& s, int role, bool, float* o) {   // (6, 7, 2), row 0 at the top
         const uint64_t mine = s.q[role], theirs = s.q[1 - role];
-        for (int r = 0; r < 6; r++)
-            for (int c = 0; c < 7; c++) {
-                const int bit = c * 7 + (5 - r), i = r * 7 + c;
-                o[2 * i] = (float)((mine >> bit) & 1ull);
-                o[2 * i + 1] = (float)((theirs >> bit) & 1ull);
-            }
+        float4* o4 = reinterpret_cast<float4*>(o);   // 84-float records: 16-byte aligned
+#pragma unroll
+        for (int i = 0; i < 42; i += 2) {   // cells i, i + 1 (row-major, row 0 at the top)
+            const int b0 = (i % 7) * 7 + (5 - i / 7), b1 = ((i + 1) % 7) * 7 + (5 - (i + 1) / 7);
+            o4[i / 2] = make_float4((float)((mine >> b0) & 1ull), (float)((theirs >> b0) & 1ull),
+                                    (float)((mine >> b1) & 1ull), (float)((theirs >> b1) & 1ull));
+        }
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int k = 0; k < 7; k++) w.u8((uint32_t)(s.q[0] >> (8 * k)) & 0xFF);
@@ -201,10 +202,12 @@ struct Othello {
         return m ? Mask128{m, 0} : Mask128{0, 1};
     }
     __device__ static void observe(const St& s, int role, bool, float* o) {   // (8, 8, 2)
-        for (int i = 0; i < 64; i++) {
-            o[2 * i] = (float)((s.q[role] >> i) & 1ull);
-            o[2 * i + 1] = (float)((s.q[1 - role] >> i) & 1ull);
-        }
+        const uint64_t mine = s.q[role], theirs = s.q[1 - role];
+        float4* o4 = reinterpret_cast<float4*>(o);   // 128-float records: 16-byte aligned
+#pragma unroll
+        for (int i = 0; i < 64; i += 2)
+            o4[i / 2] = make_float4((float)((mine >> i) & 1ull), (float)((theirs >> i) & 1ull),
+                                    (float)((mine >> (i + 1)) & 1ull), (float)((theirs >> (i + 1)) & 1ull));
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int k = 0; k < 8; k++) w.u8((uint32_t)(s.q[0] >> (8 * k)) & 0xFF);
@@ -297,13 +300,11 @@ struct Hex {
     __device__ static void observe(const St& s, int role, bool terminal, float* o) {   // (11, 11, 4)
         const U128 mine = bb(s, role), theirs = bb(s, 1 - role);
         const float swap = (!terminal && move_number(s) == 1) ? 1.0f : 0.0f;
+        float4* o4 = reinterpret_cast<float4*>(o);   // one float4 per cell (484-float records: aligned)
         for (int i = 0; i < CELLS; i++) {
             const bool m = i < 64 ? (mine.lo >> i) & 1ull : (mine.hi >> (i - 64)) & 1ull;
             const bool t = i < 64 ? (theirs.lo >> i) & 1ull : (theirs.hi >> (i - 64)) & 1ull;
-            o[4 * i] = m ? 1.0f : 0.0f;
-            o[4 * i + 1] = t ? 1.0f : 0.0f;
-            o[4 * i + 2] = (float)role;
-            o[4 * i + 3] = swap;
+            o4[i] = make_float4(m ? 1.0f : 0.0f, t ? 1.0f : 0.0f, (float)role, swap);
         }
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
@@ -379,8 +380,16 @@ struct Play2048 {
     }
     __device__ static Mask128 mask(const St& s) { return Mask128{dirs(s), 0}; }
     __device__ static void observe(const St& s, int, bool, float* o) {   // (4, 4, 31) one-hot exponents
-        for (int i = 0; i < 16; i++)
-            for (int k = 0; k < 31; k++) o[31 * i + k] = s.b[i] == k + 1 ? 1.0f : 0.0f;
+        float4* o4 = reinterpret_cast<float4*>(o);   // 496-float records: 16-byte aligned
+        for (int j = 0; j < 124; j++) {   // float 4j + t is cell (4j + t) / 31, plane (4j + t) % 31
+            float v[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int f = 4 * j + t, cell = f / 31;
+                v[t] = s.b[cell] == f - 31 * cell + 1 ? 1.0f : 0.0f;
+            }
+            o4[j] = make_float4(v[0], v[1], v[2], v[3]);
+        }
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int i = 0; i < 16; i++) w.u8(s.b[i]);
