@@ -46,10 +46,9 @@ __device__ __forceinline__ int64_t select_bit(Mask128 m, int d) {
     return (d < cl ? 0 : 64) + __ffsll((long long)w) - 1;
 }
 
+// one slot's env-core step (everything but the observation, which the warp emits)
 template <class G>
-__global__ void __launch_bounds__(128) step_kernel(Params p) {
-    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= p.n) return;
+__device__ __forceinline__ void step_slot(const Params& p, int64_t b, uint8_t* sblob, uint8_t& srole, uint8_t& sterm) {
     constexpr int P = G::P;
     const bool reset = p.force_reset || p.in.terminated[b] || p.in.truncated[b];
     const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
@@ -79,7 +78,9 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
     uint8_t* mk = p.out.legal_action_mask + b * (int64_t)G::A;
     for (int a = 0; a < G::A; a++) mk[a] = m.has(a) ? 1 : 0;
     const int role = G::role(s);
-    if (p.out.observation) G::observe(s, role, terminal, p.out.observation + b * (int64_t)G::OBS);
+    *reinterpret_cast<St*>(sblob) = s;
+    srole = (uint8_t)role;
+    sterm = terminal ? 1 : 0;
     for (int q = 0; q < P; q++) p.out.rewards[P * b + q] = r[q];
     p.out.terminated[b] = terminal;
     p.out.truncated[b] = truncated;
@@ -97,6 +98,40 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
     if (p.out.episodes && (terminal || truncated)) atomicAdd(p.out.episodes, 1ull);
 }
 
+constexpr int kWarps = 4;
+
+template <class G>
+__global__ void __launch_bounds__(kWarps * 32) step_kernel(Params p) {
+    // each warp's 32 slots' Cores are staged in shared memory so the warp can write their
+    // observation records (one contiguous region) with coalesced float4 stores
+    __shared__ __align__(16) uint8_t sblob[kWarps][32][kStateBytes];
+    __shared__ uint8_t srole[kWarps][32], sterm[kWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = ((int64_t)blockIdx.x * kWarps + warp) * 32;
+    if (base >= p.n) return;   // whole warp past the batch
+    const int64_t b = base + lane;
+    const int cnt = p.n - base < 32 ? (int)(p.n - base) : 32;
+    if (b < p.n) step_slot<G>(p, b, sblob[warp][lane], srole[warp][lane], sterm[warp][lane]);
+    __syncwarp();
+    if (p.out.observation) {
+        constexpr int OBS = G::OBS;
+        float* reg = p.out.observation + base * (int64_t)OBS;   // 16-byte aligned (base % 32 == 0)
+        const int nf = cnt * OBS;
+        for (int j = lane; 4 * j < nf; j += 32) {
+            float v[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int g = 4 * j + t, slot = g / OBS, f = g - OBS * slot;
+                v[t] = g < nf ? G::obs_at(*reinterpret_cast<const St*>(sblob[warp][slot]), srole[warp][slot],
+                                          sterm[warp][slot] != 0, f) : 0.0f;
+            }
+            if (4 * j + 3 < nf) reinterpret_cast<float4*>(reg)[j] = make_float4(v[0], v[1], v[2], v[3]);
+            else
+                for (int t = 0; t < 4 && 4 * j + t < nf; t++) reg[4 * j + t] = v[t];
+        }
+    }
+}
+
 template <class G>
 __global__ void observe_kernel(const uint8_t* blob, const uint8_t* terminated, const uint8_t* role, float* obs, int64_t n) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -109,7 +144,7 @@ __global__ void observe_kernel(const uint8_t* blob, const uint8_t* terminated, c
 template <class G>
 int launch_step(const Params& p, cudaStream_t st) {
     if (p.n <= 0) return 0;
-    step_kernel<G><<<(unsigned)((p.n + 127) / 128), 128, 0, st>>>(p);
+    step_kernel<G><<<(unsigned)((p.n + kWarps * 32 - 1) / (kWarps * 32)), kWarps * 32, 0, st>>>(p);
     return (int)cudaGetLastError();
 }
 

@@ -81,6 +81,10 @@ struct TicTacToe {
             o[2 * i + 1] = s.b[i] == 2 - role ? 1.0f : 0.0f;
         }
     }
+    // float f of the observation record (for warp-cooperative, coalesced emission)
+    __device__ static float obs_at(const St& s, int role, bool, int f) {
+        return s.b[f >> 1] == ((f & 1) ? 2 - role : role + 1) ? 1.0f : 0.0f;
+    }
     template <class W> __device__ static void encode(const St& s, W& w) { for (int i = 0; i < 10; i++) w.u8(s.b[i]); }
 };
 
@@ -122,6 +126,10 @@ struct ConnectFour {
             o4[i / 2] = make_float4((float)((mine >> b0) & 1ull), (float)((theirs >> b0) & 1ull),
                                     (float)((mine >> b1) & 1ull), (float)((theirs >> b1) & 1ull));
         }
+    }
+    __device__ static float obs_at(const St& s, int role, bool, int f) {
+        const int i = f >> 1, r = i / 7, c = i - 7 * (i / 7);
+        return (float)((s.q[(f & 1) ? 1 - role : role] >> (c * 7 + 5 - r)) & 1ull);
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int k = 0; k < 7; k++) w.u8((uint32_t)(s.q[0] >> (8 * k)) & 0xFF);
@@ -208,6 +216,9 @@ struct Othello {
         for (int i = 0; i < 64; i += 2)
             o4[i / 2] = make_float4((float)((mine >> i) & 1ull), (float)((theirs >> i) & 1ull),
                                     (float)((mine >> (i + 1)) & 1ull), (float)((theirs >> (i + 1)) & 1ull));
+    }
+    __device__ static float obs_at(const St& s, int role, bool, int f) {
+        return (float)((s.q[(f & 1) ? 1 - role : role] >> (f >> 1)) & 1ull);
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int k = 0; k < 8; k++) w.u8((uint32_t)(s.q[0] >> (8 * k)) & 0xFF);
@@ -307,6 +318,13 @@ struct Hex {
             o4[i] = make_float4(m ? 1.0f : 0.0f, t ? 1.0f : 0.0f, (float)role, swap);
         }
     }
+    __device__ static float obs_at(const St& s, int role, bool terminal, int f) {
+        const int i = f >> 2, ch = f & 3;
+        if (ch == 2) return (float)role;
+        if (ch == 3) return (!terminal && move_number(s) == 1) ? 1.0f : 0.0f;
+        const U128 x = bb(s, ch == 0 ? role : 1 - role);
+        return (float)(i < 64 ? (x.lo >> i) & 1ull : (x.hi >> (i - 64)) & 1ull);
+    }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int k = 0; k < 32; k++) w.u8(s.b[k]);   // bb0, bb1 as 16-byte little-endian integers
         w.u8(s.b[37]);
@@ -391,6 +409,10 @@ struct Play2048 {
             o4[j] = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
+    __device__ static float obs_at(const St& s, int, bool, int f) {
+        const int cell = f / 31;
+        return s.b[cell] == f - 31 * cell + 1 ? 1.0f : 0.0f;
+    }
     template <class W> __device__ static void encode(const St& s, W& w) {
         for (int i = 0; i < 16; i++) w.u8(s.b[i]);
         w.u64(s.q[2]);
@@ -434,6 +456,11 @@ struct Kuhn {
         o[s.b[role]] = 1.0f;
         o[3 + s.b[7 + role]] = 1.0f;
         o[5 + s.b[7 + 1 - role]] = 1.0f;
+    }
+    __device__ static float obs_at(const St& s, int role, bool, int f) {
+        if (f < 3) return f == s.b[role] ? 1.0f : 0.0f;
+        if (f < 5) return f - 3 == s.b[7 + role] ? 1.0f : 0.0f;
+        return f - 5 == s.b[7 + 1 - role] ? 1.0f : 0.0f;
     }
     template <class W> __device__ static void encode(const St& s, W& w) {
         w.u8(s.b[0]); w.u8(s.b[1]);
@@ -508,6 +535,12 @@ struct Leduc {
         if (s.b[2]) o[3 + s.b[2] - 1] = 1.0f;
         o[6 + s.b[5 + role]] = 1.0f;
         o[20 + s.b[5 + 1 - role]] = 1.0f;
+    }
+    __device__ static float obs_at(const St& s, int role, bool, int f) {
+        if (f < 3) return f == s.b[role] ? 1.0f : 0.0f;
+        if (f < 6) return (s.b[2] && f - 3 == s.b[2] - 1) ? 1.0f : 0.0f;
+        if (f < 20) return f - 6 == s.b[5 + role] ? 1.0f : 0.0f;
+        return f - 20 == s.b[5 + 1 - role] ? 1.0f : 0.0f;
     }
     template <class W> __device__ static void encode(const St& s, W& w) { for (int i = 0; i < 9; i++) w.u8(s.b[i]); }
 };
