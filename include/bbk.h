@@ -21,10 +21,10 @@
  * Layouts (row-major, batch leading, SURVEY §8a dtypes):
  *   observation        float32 [n, *obs_shape]  current player's view
  *   legal_action_mask  uint8   [n, A]           zero when finished
- *   rewards            float32 [n, 2]           indexed by player
+ *   rewards            float32 [n, P]           indexed by player (P = 2; the one-player 2048: 1)
  *   terminated, truncated uint8 [n]
  *   current_player, step_count int32 [n]
- *   player_to_role     int8    [n, 2]
+ *   player_to_role     int8    [n, P]
  */
 #ifndef BBK_H
 #define BBK_H
@@ -218,7 +218,7 @@ int bbk_small_observe(int game, const uint8_t* blob, const uint8_t* terminated, 
  * Device-side core.state_fingerprint (core.py:417-434) for every slot of a
  * batch: out[n, 16] = blake2b-16 of
  *   game_id | <iiBB>(current_player, step_count, terminated, truncated)
- *   | player_to_role | rewards f32[2] | packbits(mask, MSB first) | Core.encode().
+ *   | player_to_role | rewards f32[P] | packbits(mask, MSB first) | Core.encode().
  * `scratch` is [n, stride] bytes (stride = bbk_fingerprint_stride), `lens` [n].
  * batch_fingerprint (core.py:437-441) is blake2b over out[0..n) in slot order.
  * game_code: 0 Go (size = board size), 1 backgammon, 2 chess, 3 shogi, 4 small engines. */
