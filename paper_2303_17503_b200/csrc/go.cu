@@ -42,7 +42,7 @@ __host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
 // byte offset of the next board's prefetched pat (then lab) inside the scratch union:
 // past the observation and mask scratch, which are live while the prefetch is in flight
 __host__ __device__ constexpr int pf_off(int N) {
-    const int ob = 4 * (N * N + 4) + 4 * ((N * N * 17 + 31) / 32 + 2), mb = (N * N + 1 + 47) & ~15;
+    const int ob = 4 * pat_stride(N) + 4 * ((N * N * 17 + 31) / 32 + 2), mb = (N * N + 1 + 47) & ~15;
     return ((ob > mb ? ob : mb) + 15) & ~15;
 }
 
@@ -69,7 +69,7 @@ struct WarpSmem {
         } sk;
         alignas(16) uint8_t mb[((A + 47) & ~15)];
         struct {
-            uint32_t P[C + 4];
+            alignas(16) uint32_t P[pat_stride(N)];   // points C.. are padding (only feed bits >= NF)
             uint32_t W[(C * 17 + 31) / 32 + 2];
         } ob;
     } u;
@@ -378,12 +378,17 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
     constexpr int C = N * N;
     constexpr int NF = C * kPlanes;
     uint32_t* P = S.u.ob.P;
-    for (int i = lane; i < C; i += 32) {
-        uint32_t v = S.pat[i];
-        if (role) v = ((v & 0x5555u) << 1) | ((v >> 1) & 0x5555u);
-        P[i] = v | ((uint32_t)role << 16);
+    {   // 8 points per lane-iteration: black/white swapped for role 1, colour bit 16
+        const uint32_t hi = (uint32_t)role << 16;
+        for (int i = lane; i < pat_stride(N) / 8; i += 32) {
+            const uint4 v = reinterpret_cast<const uint4*>(S.pat)[i];
+            auto sw = [&](uint32_t u) { return role ? (((u & 0x55555555u) << 1) | ((u >> 1) & 0x55555555u)) : u; };
+            const uint32_t a = sw(v.x), bb = sw(v.y), c = sw(v.z), d = sw(v.w);
+            uint4* P4 = reinterpret_cast<uint4*>(P) + 2 * i;
+            P4[0] = make_uint4((a & 0xFFFFu) | hi, (a >> 16) | hi, (bb & 0xFFFFu) | hi, (bb >> 16) | hi);
+            P4[1] = make_uint4((c & 0xFFFFu) | hi, (c >> 16) | hi, (d & 0xFFFFu) | hi, (d >> 16) | hi);
+        }
     }
-    if (lane < 4) P[C + lane] = 0u;
     __syncwarp();
     // the record as a bit stream: bit f of W = float f (17 bits per point)
     uint32_t* W = S.u.ob.W;
@@ -627,14 +632,23 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             role = 1 - role;
         }
         // new transposed history: pat' = pat << 2 | current board (go.py:224, 260)
-        S.rX[lane] = Bk; S.rY[lane] = Wh;   // rowB / rowW for the pat update
-        __syncwarp();
         uint16_t* opat = p.out_s.pat + b * (int64_t)PS;
-        if (!reset) {
-            for (int i = lane; i < C; i += 32) {
-                int rr = i / N, cc = i - rr * N;
-                uint32_t v = ((uint32_t)S.pat[i] << 2) | ((S.rX[rr] >> cc) & 1u) | (((S.rY[rr] >> cc) & 1u) << 1);
-                S.pat[i] = (uint16_t)v;
+        if constexpr (N > 13) {   // row-parallel: this lane's row bits are in registers
+            if (!reset && lane < N) {
+#pragma unroll 4
+                for (int col = 0; col < N; col++) {
+                    const int i = lane * N + col;
+                    S.pat[i] = (uint16_t)(((uint32_t)S.pat[i] << 2) | ((Bk >> col) & 1u) | (((Wh >> col) & 1u) << 1));
+                }
+            }
+        } else {                  // small boards: point-parallel over all 32 lanes
+            S.rX[lane] = Bk; S.rY[lane] = Wh;
+            __syncwarp();
+            if (!reset) {
+                for (int i = lane; i < C; i += 32) {
+                    const int rr = i / N, cc = i - rr * N;
+                    S.pat[i] = (uint16_t)(((uint32_t)S.pat[i] << 2) | ((S.rX[rr] >> cc) & 1u) | (((S.rY[rr] >> cc) & 1u) << 1));
+                }
             }
         }
         __syncwarp();
