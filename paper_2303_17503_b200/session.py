@@ -7,13 +7,15 @@ random actions before step t use root.child(2t-1).
 
 from __future__ import annotations
 
+import csv
+import os
 import time
 from dataclasses import dataclass
 
 import numpy as np
 
 from .agents import random_actions_device
-from .core import Batch, batch_init, batch_step, resolve
+from .core import Batch, EngineError, batch_init, batch_step, resolve
 from .rng import RngKey
 
 
@@ -132,6 +134,22 @@ def unpack_outputs(buf) -> dict:
     return out
 
 
+class IoError(EngineError):
+    """Output path cannot be written (bench.py:28-29)."""
+
+
+@dataclass(frozen=True)
+class BenchConfig:
+    """bench.py:32-39: what bench_run measures."""
+
+    game_id: str
+    batch_size: int
+    total_steps: int
+    seed: int = 0
+    worker_threads: int | str = 1   # accepted for compatibility: the GPU grid replaces the thread pool
+    output_path: str | None = None
+
+
 @dataclass(frozen=True)
 class BenchResult:
     game_id: str
@@ -144,19 +162,74 @@ class BenchResult:
     episodes_completed: int
 
 
-def bench_run(game_id: str, batch_size: int, total_steps: int, seed: int = 0) -> BenchResult:
-    """Random-policy batched stepping with auto-reset (bench.py:109-141), on the GPU."""
+def resolve_threads(worker_threads) -> int:
+    """bench.py:54-60."""
+    if worker_threads == "auto":
+        return os.cpu_count() or 1
+    threads = int(worker_threads)
+    if threads < 1:
+        raise ValueError("worker_threads must be >= 1 or 'auto'")
+    return threads
+
+
+def bench_run(config: BenchConfig) -> BenchResult:
+    """Random-policy batched stepping with auto-reset (bench.py:63-97), on the GPU.
+
+    Wall time covers the step loop only (synchronised at both ends); the random policy is the
+    fused in-kernel sampler and episodes are counted on the device.
+    """
     import torch
 
-    sess = BatchSession(game_id, batch_size, seed, validate=False)
+    if config.batch_size < 1:
+        raise ValueError("batch_size must be >= 1")
+    if config.total_steps < 1:
+        raise ValueError("total_steps must be >= 1")
+    threads = resolve_threads(config.worker_threads)
+    sess = BatchSession(config.game_id, config.batch_size, config.seed, validate=False)
     episodes = torch.zeros(1, dtype=torch.int64, device=sess.batch._v.device)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(total_steps):
-        acts = sess.sample_random_actions()
-        b = sess.step(acts)
+    for _ in range(config.total_steps):
+        b = sess.step(sess.sample_random_actions())
         episodes += (b.device.terminated | b.device.truncated).sum()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return BenchResult(sess.gdef.game_id, batch_size, total_steps, seed, 1, wall,
-                       batch_size * total_steps / max(wall, 1e-9), int(episodes.item()))
+    samples = config.batch_size * config.total_steps
+    return BenchResult(sess.gdef.game_id, config.batch_size, config.total_steps, config.seed, threads, wall,
+                       samples / max(wall, 1e-9), int(episodes.item()))
+
+
+_BENCH_FIELDS = ("game_id", "batch_size", "total_steps", "seed", "threads", "wall_seconds", "samples_per_second",
+                 "episodes_completed")
+
+
+def _fmt(v):
+    return repr(v) if isinstance(v, float) else v   # floats round-trip exactly
+
+
+def write_results(results, path, kind: str | None = None) -> None:
+    """CSV of BenchResults with the reference's fixed header (bench.py:118-135)."""
+    rows = list(results)
+    if kind not in (None, "bench"):
+        raise ValueError("only bench results are produced here (match results need the out-of-scope agents)")
+    try:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(_BENCH_FIELDS)
+            for row in rows:
+                w.writerow([_fmt(getattr(row, f)) for f in _BENCH_FIELDS])
+    except OSError as exc:
+        raise IoError(f"cannot write {path}: {exc}") from exc
+
+
+def write_results_long(results, path) -> None:
+    """Long format, one metric per row (bench.py:138-150)."""
+    try:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(("game_id", "batch_size", "seed", "threads", "metric", "value"))
+            for row in results:
+                for metric in ("total_steps", "wall_seconds", "samples_per_second", "episodes_completed"):
+                    w.writerow((row.game_id, row.batch_size, row.seed, row.threads, metric, _fmt(getattr(row, metric))))
+    except OSError as exc:
+        raise IoError(f"cannot write {path}: {exc}") from exc

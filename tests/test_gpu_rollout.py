@@ -44,3 +44,14 @@ def test_rollout_one_player_and_small_games():
     res = bb.rollout("tic_tac_toe", 512, 2)
     assert np.all((res.lengths >= 5) & (res.lengths <= 9))
     assert set(np.unique(res.returns.sum(axis=1))) == {0.0}
+
+
+def test_bench_run_counts_episodes_like_the_session_loop():
+    """bench_run(BenchConfig) (bench.py:63-97) on the device."""
+    res = bb.bench_run(bb.BenchConfig("go_9x9", 256, 150, seed=3))
+    sess = bb.BatchSession("go_9x9", 256, 3)
+    eps = 0
+    for _ in range(150):
+        b = sess.step(sess.sample_random_actions())
+        eps += int((b.terminated | b.truncated).sum())
+    assert res.episodes_completed == eps and res.samples_per_second > 0 and res.threads == 1

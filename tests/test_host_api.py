@@ -98,3 +98,26 @@ def test_output_wire_parser_roundtrip():
     assert np.array_equal(o["observations"], a) and np.array_equal(o["legal_action_mask"], m)
     with pytest.raises(ValueError):
         unpack_outputs(b"XXXX" + bytes(60))
+
+
+def test_bench_config_results_and_csv(tmp_path):
+    """bench.py:32-60, 118-150 mirrors: validation, thread resolution and the CSV writers."""
+    from paper_2303_17503_b200.session import resolve_threads
+
+    with pytest.raises(ValueError):
+        bb.bench_run(bb.BenchConfig("go_9x9", 0, 10))
+    with pytest.raises(ValueError):
+        bb.bench_run(bb.BenchConfig("go_9x9", 4, 0))
+    assert resolve_threads("auto") >= 1 and resolve_threads(3) == 3
+    with pytest.raises(ValueError):
+        resolve_threads(0)
+    r = bb.BenchResult("go_9x9", 8, 10, 0, 1, 0.125, 640.0, 3)
+    p = tmp_path / "b.csv"
+    bb.write_results([r], p)
+    lines = p.read_text().splitlines()
+    assert lines[0] == "game_id,batch_size,total_steps,seed,threads,wall_seconds,samples_per_second,episodes_completed"
+    assert lines[1] == "go_9x9,8,10,0,1,0.125,640.0,3"
+    bb.write_results_long([r], tmp_path / "l.csv")
+    assert len((tmp_path / "l.csv").read_text().splitlines()) == 5
+    with pytest.raises(bb.IoError):
+        bb.write_results([r], tmp_path / "missing" / "x.csv")
