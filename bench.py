@@ -291,7 +291,8 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
     P = gdef.spec.num_players
     host_r = torch.empty((B, P), dtype=torch.float32, pin_memory=True)
-    host_f = torch.empty((B, 2), dtype=torch.uint8, pin_memory=True)
+    host_term = torch.empty(B, dtype=torch.bool, pin_memory=True)
+    host_trunc = torch.empty(B, dtype=torch.bool, pin_memory=True)
     host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
     t = 0
 
@@ -305,8 +306,8 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
                            next_key=root.child(2 * (t + 1) + 1))
         d = batch.device
         host_r.copy_(d.rewards, non_blocking=True)
-        host_f[:, 0].copy_(d.terminated, non_blocking=True)
-        host_f[:, 1].copy_(d.truncated, non_blocking=True)
+        host_term.copy_(d.terminated, non_blocking=True)
+        host_trunc.copy_(d.truncated, non_blocking=True)
         host_cp.copy_(d.current_player, non_blocking=True)
         host_act.copy_(random_actions_device(batch, root.child(2 * (t + 1) + 1)), non_blocking=True)
         torch.cuda.current_stream().synchronize()
