@@ -149,13 +149,25 @@ class DeviceKernel:
 
     @staticmethod
     def cols(v: DeviceV, fused: tuple | None = None) -> nat.Cols:
-        """Column pointers; `fused` = (next_key_state, next_actions tensor, episodes tensor) or None."""
-        d = v.dev
-        nk, na, ep = fused if fused is not None else (0, None, None)
-        return nat.Cols(nat.ptr(d.observation), nat.ptr(d.legal_action_mask), nat.ptr(d.rewards),
-                        nat.ptr(d.terminated), nat.ptr(d.truncated), nat.ptr(d.current_player),
-                        nat.ptr(d.step_count), nat.ptr(d.player_to_role), nat.ptr(na), int(nk) & ((1 << 64) - 1),
-                        nat.ptr(ep))
+        """Column pointers; `fused` = (next_key_state, next_actions tensor, episodes tensor) or None.
+
+        The column tensors of a DeviceV never change, so the struct is built once per batch and
+        only the fused fields are filled in per call (host overhead of the public step path)."""
+        base = v.__dict__.get("_cols")
+        if base is None:
+            d = v.dev
+            base = nat.Cols(nat.ptr(d.observation), nat.ptr(d.legal_action_mask), nat.ptr(d.rewards),
+                            nat.ptr(d.terminated), nat.ptr(d.truncated), nat.ptr(d.current_player),
+                            nat.ptr(d.step_count), nat.ptr(d.player_to_role), None, 0, None)
+            v._cols = base
+        if fused is None:
+            return base
+        nk, na, ep = fused
+        c = nat.Cols.from_buffer_copy(base)
+        c.next_actions = nat.ptr(na)
+        c.next_key = int(nk) & ((1 << 64) - 1)
+        c.episodes = nat.ptr(ep)
+        return c
 
     @staticmethod
     def _device(device):

@@ -69,7 +69,10 @@ class GoStore:
         self.lineage = None
 
     def struct(self) -> nat.GoStore:
-        return nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
+        st = self.__dict__.get("_struct")
+        if st is None:
+            st = self._struct = nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
+        return st
 
 
 class GoKernel(DeviceKernel):
@@ -98,9 +101,13 @@ class GoKernel(DeviceKernel):
         p.pass_count = torch.empty(n, dtype=torch.uint8, device=dev)
 
     def state_struct(self, v: DeviceV) -> nat.GoState:
+        st = v.__dict__.get("_gostate")   # private tensors are fixed per batch: build once
+        if st is not None:
+            return st
         p = v.priv
-        return nat.GoState(nat.ptr(p.pat), nat.ptr(p.lab), nat.ptr(p.hash), nat.ptr(p.hist_xor), nat.ptr(p.hist_len),
-                           nat.ptr(p.role_to_move), nat.ptr(p.pass_count))
+        st = v._gostate = nat.GoState(nat.ptr(p.pat), nat.ptr(p.lab), nat.ptr(p.hash), nat.ptr(p.hist_xor),
+                                      nat.ptr(p.hist_len), nat.ptr(p.role_to_move), nat.ptr(p.pass_count))
+        return st
 
     def new_store(self, n: int, limit: int, device) -> GoStore:
         torch = _torch()
