@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define BBK_ABI_VERSION 3   /* 3: bbk_go_state.lab, fingerprints, small engines */
+#define BBK_ABI_VERSION 4   /* 3: bbk_go_state.lab, fingerprints, small engines; 4: batched UCT search */
 
 typedef struct bbk_cols {
     float*    observation;        /* may be NULL: skip observation emission */
@@ -235,6 +235,85 @@ int bbk_small_fingerprint(int game, const bbk_cols* cols, const uint8_t* blob, i
                           int64_t stride, int32_t* lens, uint8_t* out, void* stream);
 /* Host build of the same blake2b-16 (pinned against hashlib by the CPU tests). */
 int bbk_blake2b16_host(const uint8_t* msg, int64_t len, uint8_t* out);
+
+/* ------------------------------------------------ batched UCT search --
+ * agents.mcts_agent (reference agents.py:49-131) for a batch of root states,
+ * one search per root, all searches advancing one simulation at a time
+ * (SURVEY §8f rank 3). The host owns the loop: per simulation
+ *   bbk_mcts_select -> bbk_copy_rows (pool -> staging) -> the game's step
+ *   kernel -> bbk_copy_rows (staging -> pool) -> bbk_mcts_untried ->
+ *   rollout: { bbk_mcts_rollout_actions -> step -> bbk_mcts_latch }* ->
+ *   bbk_mcts_backup,
+ * then bbk_mcts_best. The node pool is an ordinary batch of n_search *
+ * max_nodes slots of the game's state; node k of search s is pool row
+ * s * max_nodes + k. Each search draws from its own MT19937 stream seeded
+ * like Python's random.Random(key_state) (agents.py:85), in the reference's
+ * order, so the chosen actions are the reference's. All arrays are device
+ * memory, [n_search][max_nodes] unless noted. */
+typedef struct bbk_mcts_tree {
+    int64_t   n_search;
+    int32_t   max_nodes;       /* simulations + 1 */
+    int32_t   num_actions;     /* A */
+    int32_t   mask_words;      /* ceil(A / 32) */
+    uint32_t* mt;              /* [n_search][625]: Twister words, then the index */
+    int32_t*  visits;
+    double*   value_sum;
+    int32_t*  parent;
+    int32_t*  first_child;
+    int32_t*  last_child;
+    int32_t*  next_sibling;
+    int32_t*  action;          /* action leading to the node (-1 at the root) */
+    uint8_t*  role;            /* role to move at the node */
+    uint32_t* untried;         /* [n_search][max_nodes][mask_words] untried-action bitset */
+    int32_t*  untried_count;
+    int32_t*  next_node;       /* [n_search] */
+    int32_t*  leaf;            /* [n_search] node the current simulation ends at */
+} bbk_mcts_tree;
+
+/* Seed every search's Twister from key_states[n_search] (u64) and create its root. */
+int bbk_mcts_seed(const bbk_mcts_tree* t, const uint64_t* key_states, void* stream);
+/* Untried set and role of node[s] (node == NULL: the root) of every search from
+ * staging row s's mask / current_player / player_to_role; node[s] < 0 skips. */
+int bbk_mcts_untried(const bbk_mcts_tree* t, const uint8_t* mask, const int32_t* current_player,
+                     const int8_t* player_to_role, const int32_t* node, void* stream);
+/* Selection + expansion (agents.py:89-109) with exploration constant c and
+ * log_table[v] = log(v) for v <= max_nodes. Outputs per search: src_row (pool
+ * row to step from), dst_row (pool row of the new child, -1 if the selected node
+ * is finished), actions, new_node (-1 likewise). */
+int bbk_mcts_select(const bbk_mcts_tree* t, double c, const double* log_table, int32_t* src_row, int32_t* dst_row,
+                    int64_t* actions, int32_t* new_node, void* stream);
+/* Rollout moves (agents.py:113-116) from staging masks [n_search, A]; done[s] != 0: lowest legal. */
+int bbk_mcts_rollout_actions(const bbk_mcts_tree* t, const uint8_t* mask, const uint8_t* done, int64_t* actions,
+                             void* stream);
+/* Role rewards of rollouts that just ended (agents.py:117, 126-131) into role_returns [n, 2];
+ * sel != NULL restricts to slots with (sel[s] >= 0) == (want != 0). */
+int bbk_mcts_latch(const uint8_t* terminated, const uint8_t* truncated, const float* rewards,
+                   const int8_t* player_to_role, const int32_t* sel, int want, int64_t n, uint8_t* done,
+                   float* role_returns, unsigned long long* count, void* stream);
+/* Backup (agents.py:117-122): value_sum += scale * role_return[mover] + offset along each path. */
+int bbk_mcts_backup(const bbk_mcts_tree* t, const float* role_returns, double scale, double offset, void* stream);
+/* Most visited root child, ties to the lowest action (agents.py:124-129). */
+int bbk_mcts_best(const bbk_mcts_tree* t, int64_t* actions, void* stream);
+
+/* Row gather / scatter of up to BBK_ROW_COPY_MAX per-slot tensors at once:
+ * dst[dst_idx[i]] = src[src_idx[i]] (index NULL = i; a negative index skips
+ * row i), rows of row_bytes moved in units of `unit` (1, 4, 8 or 16) bytes. */
+#define BBK_ROW_COPY_MAX 24
+typedef struct bbk_row_copy {
+    const void* src;
+    void*       dst;
+    int64_t     row_bytes;
+    int64_t     unit;
+} bbk_row_copy;
+typedef struct bbk_row_copy_set {
+    int32_t      count;
+    bbk_row_copy t[BBK_ROW_COPY_MAX];
+} bbk_row_copy_set;
+int bbk_copy_rows(const bbk_row_copy_set* set, const int32_t* src_idx, const int32_t* dst_idx, int64_t n,
+                  void* stream);
+/* Host twin of the device Twister (CPU tests against Python's random):
+ * out[i] = randrange(below[i]) on random.Random(seed), or a raw 32-bit word when below[i] == 0. */
+int bbk_mt19937_host(uint64_t seed, const uint32_t* below, int64_t n, uint32_t* out);
 
 #ifdef __cplusplus
 }

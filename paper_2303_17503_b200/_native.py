@@ -58,6 +58,24 @@ class ShogiState(C.Structure):
     _fields_ = [("board", P), ("misc", P), ("hist", P), ("hist_cap", I32)]
 
 
+class MctsTree(C.Structure):
+    _fields_ = [("n_search", I64), ("max_nodes", I32), ("num_actions", I32), ("mask_words", I32), ("mt", P),
+                ("visits", P), ("value_sum", P), ("parent", P), ("first_child", P), ("last_child", P),
+                ("next_sibling", P), ("action", P), ("role", P), ("untried", P), ("untried_count", P),
+                ("next_node", P), ("leaf", P)]
+
+
+ROW_COPY_MAX = 24   # BBK_ROW_COPY_MAX
+
+
+class RowCopy(C.Structure):
+    _fields_ = [("src", P), ("dst", P), ("row_bytes", I64), ("unit", I64)]
+
+
+class RowCopySet(C.Structure):
+    _fields_ = [("count", I32), ("t", RowCopy * ROW_COPY_MAX)]
+
+
 def _declare(L):
     """ctypes signatures. A symbol missing from an older library build (A/B runs with BBK_LIB)
     is skipped here; tests/test_abi.py checks that the in-tree build exports all of include/bbk.h."""
@@ -101,6 +119,15 @@ def _declare(L):
     sig("bbk_small_init", [C.c_int, ptr(Cols), P, I64, I64, U64, P, I32, P])
     sig("bbk_small_step", [C.c_int, ptr(Cols), P, ptr(Cols), P, P, I64, I64, U64, P, I32, P])
     sig("bbk_small_observe", [C.c_int, P, P, P, P, I64, P])
+    sig("bbk_mcts_seed", [ptr(MctsTree), P, P])
+    sig("bbk_mcts_untried", [ptr(MctsTree), P, P, P, P, P])
+    sig("bbk_mcts_select", [ptr(MctsTree), C.c_double, P, P, P, P, P, P])
+    sig("bbk_mcts_rollout_actions", [ptr(MctsTree), P, P, P, P])
+    sig("bbk_mcts_latch", [P, P, P, P, P, C.c_int, I64, P, P, P, P])
+    sig("bbk_mcts_backup", [ptr(MctsTree), P, C.c_double, C.c_double, P])
+    sig("bbk_mcts_best", [ptr(MctsTree), P, P])
+    sig("bbk_copy_rows", [ptr(RowCopySet), P, P, I64, P])
+    sig("bbk_mt19937_host", [U64, P, I64, P])
     return L
 
 

@@ -1,6 +1,9 @@
-"""Random-policy sampling (reference agents.py:25-46) on the device."""
+"""Agents (reference agents.py): random sampling, batched rollouts, UCT search and matches on the device."""
 
 from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
 
 import numpy as np
 
@@ -80,3 +83,146 @@ def rollout(game, n: int, seed: int, *, max_steps: int | None = None, check_ever
             if int(count.item()) >= n:
                 break
     return RolloutResult(sess.gdef.game_id, ret.cpu().numpy(), length.cpu().numpy(), t)
+
+
+# ----------------------------------------------------------------- search agents and matches
+from .search import mcts_actions, mcts_agent  # noqa: E402  (batched UCT search, agents.py:63-123)
+
+
+@dataclass(frozen=True)
+class MatchResult:
+    """Aggregate outcome of one pairing (reference elo.py:22-35)."""
+
+    game_id: str
+    agent_a: str
+    agent_b: str
+    wins_a: int
+    wins_b: int
+    draws: int
+
+    @property
+    def total(self) -> int:
+        return self.wins_a + self.wins_b + self.draws
+
+
+@dataclass(frozen=True)
+class AgentPolicy:
+    """A named decision function (agents.py:134-144). ``simulations`` marks the UCT agent, which
+    the batched match runner searches on the device for all its games at once."""
+
+    name: str
+    fn: Callable
+    requires_perfect_information: bool = False
+    simulations: int = 0
+
+    def __call__(self, state: EnvState, key: RngKey) -> int:
+        return self.fn(state, key)
+
+
+def random_policy() -> AgentPolicy:
+    return AgentPolicy("random", random_agent)
+
+
+def mcts_policy(simulations: int = 32) -> AgentPolicy:
+    def fn(state, key):
+        return mcts_agent(state, key, simulations)
+
+    return AgentPolicy(f"mcts{simulations}", fn, requires_perfect_information=True, simulations=simulations)
+
+
+def _keys_at(states: np.ndarray, index: int) -> np.ndarray:
+    from .rng import child_states_at
+
+    return child_states_at(states, index)
+
+
+def _random_choice(mask: np.ndarray, key_states: np.ndarray) -> np.ndarray:
+    """random_agent per row: legal[key.randint(len(legal))] (agents.py:25-30); 0 for empty rows."""
+    cnt = mask.sum(axis=1).astype(np.uint64)
+    d = key_states.astype(np.uint64) % np.maximum(cnt, 1)
+    cum = np.cumsum(mask, axis=1, dtype=np.int64)
+    act = (cum <= d[:, None].astype(np.int64)).sum(axis=1)
+    act[cnt == 0] = 0
+    return act.astype(np.int64)
+
+
+def play_games(game, players: tuple, keys) -> tuple:
+    """``play_game(gdef, players, key)`` (agents.py:163-172) for every key at once, one slot per
+    game: (rewards [G, 2], step_count [G]) of each game's final state. Games advance in lockstep; UCT moves of all
+    games whose player to move is the same search agent are one batched device search."""
+    from .core import resolve
+    from .rng import key_state
+
+    gdef = resolve(game)
+    kern = gdef.batch_kernel
+    g = len(keys)
+    ks = np.asarray([key_state(k) for k in keys], dtype=np.uint64)
+    limit = gdef.max_steps
+    v = kern.init(gdef, None, g, limit, slot_keys=_keys_at(ks, 0).tolist())
+    done = np.zeros(g, dtype=bool)
+    final = np.zeros((g, gdef.spec.num_players), dtype=np.float32)
+    length = np.zeros(g, dtype=np.int32)
+    t = 0
+    pools = {}
+    while True:
+        fin = np.asarray(v.terminated, dtype=bool) | np.asarray(v.truncated, dtype=bool)
+        fresh = fin & ~done
+        if fresh.any():
+            final[fresh] = np.asarray(v.rewards)[fresh]
+            length[fresh] = np.asarray(v.step_count)[fresh]
+            done |= fresh
+        if done.all():
+            return final, length
+        t += 1
+        akeys = _keys_at(ks, 2 * t - 1)
+        mask = np.asarray(v.legal_action_mask, dtype=bool)
+        acts = _random_choice(mask, akeys)          # random agents, and the games already over
+        cur = np.asarray(v.current_player)
+        for p, agent in enumerate(players):
+            if agent.simulations <= 0:
+                if agent.fn is not random_agent:
+                    raise ValueError(f"agent {agent.name!r} has no batched device form")
+                continue
+            rows = np.flatnonzero(~done & ~fin & (cur == p))
+            if rows.size:
+                acts[rows] = mcts_search_rows(v, rows, akeys[rows], agent.simulations, pools, p)
+        v = kern.step(gdef, v, acts, None, limit, validate=True, slot_keys=_keys_at(ks, 2 * t).tolist())
+
+
+def mcts_search_rows(v, rows, key_states, simulations, pools, tag):
+    from . import search
+
+    pool = pools.get((tag, len(rows)))
+    if pool is None or not pool.fits(v.kern, v, len(rows), simulations):
+        pool = search.SearchPool(v.kern, v, len(rows), simulations)
+        pools[(tag, len(rows))] = pool
+    return search.search(v, rows.tolist(), [int(k) for k in key_states], simulations, pool=pool).cpu().numpy()
+
+
+def run_matches(game, agents: list, games_per_pair: int, key: RngKey) -> list:
+    """Round-robin pairwise matches (agents.py:175-216) with every pairing's games played in
+    parallel on the device; identical results to the reference's sequential runner."""
+    from .core import UnsupportedGame, resolve
+
+    gdef = resolve(game)
+    if len(agents) < 2:
+        raise ValueError("run_matches needs at least two agents")
+    chance_or_hidden = gdef.chance_in_step or not gdef.perfect_information
+    for agent in agents:
+        if agent.requires_perfect_information and (chance_or_hidden or gdef.spec.num_players != 2):
+            raise UnsupportedGame(f"{agent.name} does not support {gdef.game_id}")
+    if gdef.spec.num_players != 2:
+        raise UnsupportedGame(f"run_matches supports 2-player games, not {gdef.game_id}")
+    if games_per_pair == 0:
+        return []
+    results = []
+    pair_index = 0
+    for i in range(len(agents)):
+        for j in range(i + 1, len(agents)):
+            pair_key = key.child(pair_index)
+            pair_index += 1
+            final, _ = play_games(gdef, (agents[i], agents[j]), [pair_key.child(g) for g in range(games_per_pair)])
+            r0 = final[:, 0]
+            results.append(MatchResult(gdef.game_id, agents[i].name, agents[j].name, int((r0 > 0).sum()),
+                                       int((r0 < 0).sum()), int((r0 == 0).sum())))
+    return results

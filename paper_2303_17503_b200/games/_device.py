@@ -374,6 +374,32 @@ class DeviceKernel:
                                                nat.stream_handle(v.device)), "bbk_random_actions")
         return out
 
+    # ---------------------------------------------- whole-row copies (search pools)
+    def row_tensors(self, v: DeviceV) -> list:
+        """Every per-slot tensor of a batch's state (columns except the observation, private
+        state, per-env stores), leading dimension n: what a slot IS, for bbk_copy_rows."""
+        d = v.dev
+        out = [d.legal_action_mask, d.rewards, d.terminated, d.truncated, d.current_player, d.step_count,
+               d.player_to_role]
+        out += list(vars(v.priv).values())
+        if v.store is not None:
+            out += v.store.row_tensors()
+        return out
+
+    def new_v_like(self, v: DeviceV, n: int, store: bool = True) -> DeviceV:
+        """A batch of n slots with v's state layout (no observation), with its own stores."""
+        w = self.new_v(n, 0, v.device, v.t, v.limit, obs=False)
+        w.store = None if (v.store is None or not store) else v.store.like(n)
+        return w
+
+    def raw_step(self, v: DeviceV, out: DeviceV, a, limit: int, slot_keys=None) -> None:
+        """The step kernel on buffers the caller owns: no validation, no lineage bookkeeping;
+        v and out share v's per-env store (updated in place)."""
+        out.store = v.store
+        out._host = {}
+        self._fused = None
+        self.launch_step(v, out, a, 0, slot_keys, limit)
+
     # subclasses
     def launch_init(self, v, ks, sk):
         raise NotImplementedError

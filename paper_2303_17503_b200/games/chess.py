@@ -30,6 +30,14 @@ class RingStore:
         self.hist = hist
         self.lineage = None
 
+    def row_tensors(self):
+        return [self.hist]
+
+    def like(self, n: int) -> "RingStore":
+        torch = _torch()
+        return RingStore(torch.empty((n,) + tuple(self.hist.shape[1:]), dtype=self.hist.dtype,
+                                     device=self.hist.device))
+
 
 class ChessCoreView:
     __slots__ = ("board", "role_to_move", "castling", "ep", "halfmove", "rep", "terminal", "rewards", "mask")

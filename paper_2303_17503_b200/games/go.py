@@ -68,6 +68,15 @@ class GoStore:
         self.hist_cap = hist_cap
         self.lineage = None
 
+    def row_tensors(self):
+        return [self.history, self.bloom]
+
+    def like(self, n: int) -> "GoStore":
+        torch = _torch()
+        return GoStore(torch.empty((n, self.hist_cap), dtype=torch.int64, device=self.history.device),
+                       torch.empty((n,) + tuple(self.bloom.shape[1:]), dtype=self.bloom.dtype,
+                                   device=self.bloom.device), self.hist_cap)
+
     def struct(self) -> nat.GoStore:
         st = self.__dict__.get("_struct")
         if st is None:

@@ -8,7 +8,13 @@ HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def names():
-    return sorted(f[:-5] for f in os.listdir(HERE) if f.endswith(".json"))
+    """Trajectory fixtures (make_golden*.py); the search fixtures are listed by search_names()."""
+    return sorted(f[:-5] for f in os.listdir(HERE) if f.endswith(".json") and not f.startswith("mcts_"))
+
+
+def search_names():
+    """UCT-search decision fixtures (make_golden_mcts.py)."""
+    return sorted(f[:-5] for f in os.listdir(HERE) if f.endswith(".json") and f.startswith("mcts_"))
 
 
 def load(name):

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     L = _native.lib()
     missing = [s for s in declared_symbols() if not hasattr(L, s)]
     assert not missing, missing
-    assert L.bbk_abi_version() == 3
+    assert L.bbk_abi_version() == 4
 
 
 def test_library_is_sm100a():
