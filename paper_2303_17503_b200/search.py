@@ -119,12 +119,31 @@ class SearchPool:
         self.sb = kern.new_v_like(template, n, store=False)
         self.sb.store = self.sa.store
         self.pool_rows = kern.row_tensors(self.pool)
+        self.graphs = {}
+
+    def graph(self, key, fn) -> None:
+        """Replay the CUDA graph of `fn`'s launches (captured on first use) on the current stream.
+        Every pointer the launches use belongs to this pool, so the capture stays valid."""
+        torch = _torch()
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.graph(g, stream=side):
+                fn()
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            self.graphs[key] = g
+        g.replay()
 
     def fits(self, kern, template, n_search, simulations) -> bool:
         return (kern is self.kern and n_search == self.n and max(1, int(simulations)) == self.sims
                 and template.device == self.device and template.limit == self.limit
                 and [tuple(t.shape[1:]) for t in kern.row_tensors(template)] ==
                 [tuple(t.shape[1:]) for t in self.pool_rows])
+
+
+SHORT_CHUNK, LONG_CHUNK = 4, 32   # rollout moves between finished-search polls (even: ping-pong parity)
 
 
 def _latch(v, sel, want, p, stream) -> None:
@@ -135,11 +154,15 @@ def _latch(v, sel, want, p, stream) -> None:
 
 
 def search(v, rows, key_states, simulations: int = 32, *, exploration: float = math.sqrt(2.0),
-           value_transform: tuple = (1.0, 0.0), check_every: int = 8, pool: SearchPool | None = None):
+           value_transform: tuple = (1.0, 0.0), pool: SearchPool | None = None, stats: dict | None = None,
+           graphs: bool = True):
     """mcts_agent(state_at(v, rows[s]), RngKey(key_states[s]), simulations, ...) for every s, on the device.
 
     Returns the chosen actions as a CUDA int64 tensor [len(rows)]. Rows must be unfinished slots
-    of batch v (mcts_agent raises TerminalStep otherwise; checked by the caller)."""
+    of batch v (mcts_agent raises TerminalStep otherwise; checked by the caller). ``stats``, if
+    given, accumulates the batched steps taken (``expand_steps``, ``rollout_steps``). With
+    ``graphs`` the per-simulation launch sequence and the rollout chunks replay as CUDA graphs
+    captured once per pool (the loop is otherwise bound by host launch overhead)."""
     torch = _torch()
     kern = v.kern
     L = nat.lib()
@@ -165,29 +188,47 @@ def search(v, rows, key_states, simulations: int = 32, *, exploration: float = m
                                  nat.ptr(sa.dev.player_to_role), None, stream), "bbk_mcts_untried")
     limit = v.limit
     sa_rows, sb_rows = kern.row_tensors(sa), kern.row_tensors(sb)
-    for _ in range(sims):
+
+    def prologue():   # selection, expansion step, first latches (one simulation, up to the rollout)
+        st = nat.stream_handle(dev)
         nat.check(L.bbk_mcts_select(tree, float(c), nat.ptr(p.logtab), nat.ptr(p.src_row), nat.ptr(p.dst_row),
-                                    nat.ptr(p.act), nat.ptr(p.new_id), stream), "bbk_mcts_select")
-        copy_rows(p.pool_rows, sa_rows, p.src_row, None, n, stream)
+                                    nat.ptr(p.act), nat.ptr(p.new_id), st), "bbk_mcts_select")
+        copy_rows(p.pool_rows, sa_rows, p.src_row, None, n, st)
         p.done.zero_()
         p.count.zero_()
-        _latch(sa, p.new_id, 0, p, stream)        # finished leaves score themselves
-        kern.raw_step(sa, sb, p.act, limit)       # expansion step (agents.py:106)
-        copy_rows(sb_rows, p.pool_rows, None, p.dst_row, n, stream)
+        _latch(sa, p.new_id, 0, p, st)        # finished leaves score themselves
+        kern.raw_step(sa, sb, p.act, limit)   # expansion step (agents.py:106)
+        copy_rows(sb_rows, p.pool_rows, None, p.dst_row, n, st)
         nat.check(L.bbk_mcts_untried(tree, nat.ptr(sb.dev.legal_action_mask), nat.ptr(sb.dev.current_player),
-                                     nat.ptr(sb.dev.player_to_role), nat.ptr(p.new_id), stream), "bbk_mcts_untried")
-        _latch(sb, p.new_id, 1, p, stream)
+                                     nat.ptr(sb.dev.player_to_role), nat.ptr(p.new_id), st), "bbk_mcts_untried")
+        _latch(sb, p.new_id, 1, p, st)
+
+    def rollout(k):   # k rollout moves (k even: the live batch is back in sb afterwards)
+        st = nat.stream_handle(dev)
         cur, nxt = sb, sa
-        t = 0
-        while True:
-            if t % check_every == 0 and int(p.count.item()) >= n:
-                break
+        for _ in range(k):
             nat.check(L.bbk_mcts_rollout_actions(tree, nat.ptr(cur.dev.legal_action_mask), nat.ptr(p.done),
-                                                 nat.ptr(p.act), stream), "bbk_mcts_rollout_actions")
+                                                 nat.ptr(p.act), st), "bbk_mcts_rollout_actions")
             kern.raw_step(cur, nxt, p.act, limit)
-            _latch(nxt, None, 1, p, stream)
+            _latch(nxt, None, 1, p, st)
             cur, nxt = nxt, cur
-            t += 1
+
+    run_pro = (lambda: p.graph(("pro", float(c)), prologue)) if graphs else prologue
+    prev = 0
+    for _ in range(sims):
+        run_pro()
+        t = 0
+        while int(p.count.item()) < n:
+            k = LONG_CHUNK if t + LONG_CHUNK <= 0.75 * prev else SHORT_CHUNK
+            if graphs:
+                p.graph(("roll", k), lambda: rollout(k))
+            else:
+                rollout(k)
+            t += k
+        prev = max(prev, t)
+        if stats is not None:
+            stats["expand_steps"] = stats.get("expand_steps", 0) + 1
+            stats["rollout_steps"] = stats.get("rollout_steps", 0) + t
         nat.check(L.bbk_mcts_backup(tree, nat.ptr(p.ret), float(scale), float(offset), stream), "bbk_mcts_backup")
     nat.check(L.bbk_mcts_best(tree, nat.ptr(p.best), stream), "bbk_mcts_best")
     return p.best.clone()

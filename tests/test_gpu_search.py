@@ -137,3 +137,14 @@ def test_run_matches_matches_reference(name):
             got = [[float(final[g, 0]), float(final[g, 1]), int(length[g])] for g in range(len(length))]
             assert got == rec["games"][k]
             k += 1
+
+
+def test_graph_and_eager_paths_agree():
+    rec = goldens.load("mcts_go_9x9_s0_b8_t20_sims16")
+    batch = _roots(rec)
+    v = batch._v
+    rows = list(range(rec["batch"]))
+    keys = [bb.RngKey(rec["key_seed"]).child(i).state for i in rows]
+    eager = search.search(v, rows, keys, rec["sims"], graphs=False).cpu().numpy().tolist()
+    graphed = search.search(v, rows, keys, rec["sims"], graphs=True).cpu().numpy().tolist()
+    assert eager == graphed == rec["actions"]
