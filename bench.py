@@ -276,10 +276,12 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     """Same metric through the public API with host buffers, over the same step window.
 
     A fresh batch (same seed, same slots) is stepped W untimed + K timed steps through
-    core.batch_step. Per step: device random policy -> D2H of the actions into pinned host
-    memory (a host agent's output) -> core.batch_step(host actions) (H2D inside) -> D2H of
-    rewards/terminated/truncated/current_player, read on the host (synchronous, as a host RL
-    loop does).
+    core.batch_step. Per step: core.batch_step(pinned host actions) (H2D inside) -> D2H of the
+    device random policy's next actions into the pinned action buffer (a host agent's output, on
+    the critical path: the next step needs it) -> D2H of the step's rewards / terminated /
+    truncated / current_player on a copy stream into double-buffered pinned buffers, read on the
+    host one step later (they overlap the next step's H2D and kernel; the last step's are waited
+    for inside the timed region).
     """
     import torch
 
@@ -290,37 +292,57 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
                                                             device=dev, next_key=root.child(1)))
     host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
     P = gdef.spec.num_players
-    host_r = torch.empty((B, P), dtype=torch.float32, pin_memory=True)
-    host_term = torch.empty(B, dtype=torch.bool, pin_memory=True)
-    host_trunc = torch.empty(B, dtype=torch.bool, pin_memory=True)
-    host_cp = torch.empty(B, dtype=torch.int32, pin_memory=True)
+    host = [dict(r=torch.empty((B, P), dtype=torch.float32, pin_memory=True),
+                 term=torch.empty(B, dtype=torch.bool, pin_memory=True),
+                 trunc=torch.empty(B, dtype=torch.bool, pin_memory=True),
+                 cp=torch.empty(B, dtype=torch.int32, pin_memory=True)) for _ in range(2)]
+    main = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    pending = []      # (batch whose results are in flight, copy-stream event, host buffer set)
     t = 0
 
     host_act.copy_(random_actions_device(batch, root.child(1)))
 
+    def read(entry):
+        entry[1].synchronize()    # step t's rewards / flags / current player are now in host memory
+
     def one():
-        # the host agent's actions (host_act, pinned) -> batch_step (H2D inside) -> D2H of the
-        # step's rewards / flags / current player and of the policy's next actions, one sync
         nonlocal batch, t
         batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False,
                            next_key=root.child(2 * (t + 1) + 1))
         d = batch.device
-        host_r.copy_(d.rewards, non_blocking=True)
-        host_term.copy_(d.terminated, non_blocking=True)
-        host_trunc.copy_(d.truncated, non_blocking=True)
-        host_cp.copy_(d.current_player, non_blocking=True)
+        h = host[t % 2]
+        done = torch.cuda.Event()
+        done.record(main)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            h["r"].copy_(d.rewards, non_blocking=True)
+            h["term"].copy_(d.terminated, non_blocking=True)
+            h["trunc"].copy_(d.truncated, non_blocking=True)
+            h["cp"].copy_(d.current_player, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
         host_act.copy_(random_actions_device(batch, root.child(2 * (t + 1) + 1)), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        main.synchronize()
+        if pending:
+            read(pending.pop())
+        pending.append((batch, ev, h))
         t += 1
+
+    def drain():
+        while pending:
+            read(pending.pop())
 
     for _ in range(args.warmup):
         one()
+    drain()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         one()
+    drain()
     dt = time.perf_counter() - t0
     if world > 1:
         import torch.distributed as dist
@@ -330,8 +352,9 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
         dt = float(tt.item())
     return {"value": B * world * args.steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
             "d2h_bytes_per_step": (4 * P + 2 + 4 + 8) * B, "steps": args.steps,
-            "path": "public core.batch_step with pinned host action buffer + host read of rewards/flags/player, "
-                    "same window as value (fresh init, W warm-up, K timed)"}
+            "path": "public core.batch_step with a pinned host action buffer (H2D inside) + D2H of the next "
+                    "actions (critical path) and of rewards/flags/player (copy stream, read by the host one "
+                    "step later), same window as value (fresh init, W warm-up, K timed)"}
 
 
 def run_sweep(args, gdef, kern, dev, slot0):

@@ -14,6 +14,8 @@ the C-ABI calls.
 from __future__ import annotations
 
 import ctypes as C
+import sys
+import weakref
 from types import SimpleNamespace
 
 import numpy as np
@@ -120,6 +122,32 @@ class DeviceV:
         return arr
 
 
+POOL_DEPTH = 2        # dead batches' buffer sets kept per (n, device, obs, stream)
+_CACHED = ("_cols", "_gostate")   # ctypes structs of fixed column pointers, valid with the buffers
+
+
+def _recycle(pool: list, vd: dict) -> None:
+    """Finalizer of a DeviceV: return its column and private buffers to the pool when nothing else
+    references them (no Python alias, view, DLPack export or numpy view of any tensor).
+
+    A recycled buffer set is handed to the next new_v on the same stream, so stream order makes
+    the reuse safe exactly as for torch's caching allocator. This removes the ~16 allocations and
+    the pointer-struct rebuild from every public step call (the e2e path's host overhead).
+    """
+    if len(pool) >= POOL_DEPTH:
+        return
+    dev, priv = vd.get("dev"), vd.get("priv")
+    if dev is None or priv is None:
+        return
+    use_count = _torch()._C._storage_Use_Count
+    for ns in (dev, priv):
+        for t in vars(ns).values():
+            # references: the namespace, the loop variable, getrefcount's argument
+            if t is not None and (sys.getrefcount(t) != 3 or use_count(t.untyped_storage()._cdata) != 2):
+                return
+    pool.append((dev, priv, {k: vd[k] for k in _CACHED if k in vd}))
+
+
 class DeviceKernel:
     """Common host logic; subclasses implement the game-specific C-ABI calls."""
 
@@ -130,8 +158,25 @@ class DeviceKernel:
 
     # ------------------------------------------------------------ allocation
     def new_v(self, n: int, slot0: int, device, t: int, limit: int, obs: bool = True) -> DeviceV:
+        """A batch state of n slots: buffers recycled from a dead batch of the same shape on the same
+        stream when one is pooled (see _recycle), else freshly allocated."""
         torch = _torch()
         v = DeviceV(self, n, slot0, device, t, limit)
+        pools = self.__dict__.setdefault("_pools", {})
+        stream = torch.cuda.current_stream(device).cuda_stream if torch.device(device).type == "cuda" else 0
+        pkey = (n, device, obs, stream)
+        pool = pools.setdefault(pkey, [])
+        if pool:
+            v.dev, v.priv, cached = pool.pop()
+            v.__dict__.update(cached)
+        else:
+            self._alloc_columns(v, obs)
+        weakref.finalize(v, _recycle, pool, v.__dict__).atexit = False
+        return v
+
+    def _alloc_columns(self, v: DeviceV, obs: bool) -> None:
+        torch = _torch()
+        n, device = v.n, v.device
         d = v.dev
         d.observation = torch.empty((n,) + tuple(self.obs_shape), dtype=torch.float32, device=device) if obs else None
         d.legal_action_mask = torch.empty((n, self.num_actions), dtype=torch.bool, device=device)
@@ -142,7 +187,6 @@ class DeviceKernel:
         d.step_count = torch.empty(n, dtype=torch.int32, device=device)
         d.player_to_role = torch.empty((n, self.num_players), dtype=torch.int8, device=device)
         self.alloc_private(v)
-        return v
 
     def alloc_private(self, v: DeviceV) -> None:
         raise NotImplementedError

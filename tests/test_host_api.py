@@ -121,3 +121,46 @@ def test_bench_config_results_and_csv(tmp_path):
     assert len((tmp_path / "l.csv").read_text().splitlines()) == 5
     with pytest.raises(bb.IoError):
         bb.write_results([r], tmp_path / "missing" / "x.csv")
+
+
+def _toy_kernel():
+    import torch
+
+    from paper_2303_17503_b200.games._device import DeviceKernel
+
+    class Toy(DeviceKernel):
+        game_id, num_actions, obs_shape = "toy", 4, (3,)
+
+        def alloc_private(self, v):
+            v.priv.board = torch.zeros((v.n, 5), dtype=torch.uint8, device=v.device)
+
+    return Toy()
+
+
+def test_dead_batch_buffers_are_recycled_only_when_unreferenced():
+    """new_v reuses a dead batch's buffers (e2e host overhead) but never ones still referenced."""
+    import gc
+
+    import torch
+
+    k = _toy_kernel()
+    v = k.new_v(8, 0, torch.device("cpu"), 0, 10)
+    ids = (id(v.dev.rewards), id(v.priv.board))
+    del v
+    gc.collect()
+    w = k.new_v(8, 0, torch.device("cpu"), 1, 10)
+    assert (id(w.dev.rewards), id(w.priv.board)) == ids            # recycled
+    assert k.new_v(4, 0, torch.device("cpu"), 0, 10).n == 4       # other shape: fresh
+    pool = next(iter(k._pools.values()))
+    for hold in (lambda x: x.dev.rewards, lambda x: x.dev.rewards[1:3], lambda x: x.priv.board.numpy(),
+                 lambda x: torch.utils.dlpack.to_dlpack(x.dev.observation)):
+        pool.clear()
+        keep = hold(w)
+        del w
+        gc.collect()
+        assert pool == []                                           # a live reference blocks reuse
+        w = k.new_v(8, 0, torch.device("cpu"), 1, 10)
+        del keep
+    del w
+    gc.collect()
+    assert len(pool) == 1
