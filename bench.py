@@ -276,12 +276,12 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     """Same metric through the public API with host buffers, over the same step window.
 
     A fresh batch (same seed, same slots) is stepped W untimed + K timed steps through
-    core.batch_step. Per step: core.batch_step(pinned host actions) (H2D inside) -> D2H of the
-    device random policy's next actions into the pinned action buffer (a host agent's output, on
-    the critical path: the next step needs it) -> D2H of the step's rewards / terminated /
-    truncated / current_player on a copy stream into double-buffered pinned buffers, read on the
-    host one step later (they overlap the next step's H2D and kernel; the last step's are waited
-    for inside the timed region).
+    core.batch_step. Per step: core.batch_step reads the host agent's actions from a pinned host
+    buffer and its fused sampler writes the device random policy's next actions into the other
+    pinned buffer (zero-copy over PCIe: the kernel loads / stores them itself; BBK_ZERO_COPY=0 uses
+    an H2D copy and a D2H copy instead); the step's rewards / terminated / truncated /
+    current_player go D2H on a copy stream into double-buffered pinned buffers, read on the host one
+    step later (they overlap the next step; the last step's are waited for inside the timed region).
     """
     import torch
 
@@ -290,7 +290,9 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
 
     batch = Batch(gdef, B, gdef.max_steps, vstate=kern.init(gdef, root.child(0), B, gdef.max_steps, slot0=slot0,
                                                             device=dev, next_key=root.child(1)))
-    host_act = torch.empty(B, dtype=torch.int64, pin_memory=True)
+    # the host agent's action buffers (pinned, ping-pong): step t reads acts[t % 2] in place and its
+    # fused sampler writes the next actions into acts[(t + 1) % 2] (zero-copy both ways)
+    acts = [torch.empty(B, dtype=torch.int64, pin_memory=True) for _ in range(2)]
     P = gdef.spec.num_players
     host = [dict(r=torch.empty((B, P), dtype=torch.float32, pin_memory=True),
                  term=torch.empty(B, dtype=torch.bool, pin_memory=True),
@@ -301,15 +303,20 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
     pending = []      # (batch whose results are in flight, copy-stream event, host buffer set)
     t = 0
 
-    host_act.copy_(random_actions_device(batch, root.child(1)))
+    acts[0].copy_(random_actions_device(batch, root.child(1)))
 
     def read(entry):
         entry[1].synchronize()    # step t's rewards / flags / current player are now in host memory
 
+    from paper_2303_17503_b200.games._device import ZERO_COPY
+
     def one():
         nonlocal batch, t
-        batch = batch_step(batch, host_act, root.child(2 * (t + 1)), validate=False,
-                           next_key=root.child(2 * (t + 1) + 1))
+        nk = root.child(2 * (t + 1) + 1)
+        batch = batch_step(batch, acts[t % 2], root.child(2 * (t + 1)), validate=False, next_key=nk,
+                           next_actions=acts[(t + 1) % 2] if ZERO_COPY else None)
+        if not ZERO_COPY:
+            acts[(t + 1) % 2].copy_(random_actions_device(batch, nk), non_blocking=True)
         d = batch.device
         h = host[t % 2]
         done = torch.cuda.Event()
@@ -322,8 +329,7 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
             h["cp"].copy_(d.current_player, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
-        host_act.copy_(random_actions_device(batch, root.child(2 * (t + 1) + 1)), non_blocking=True)
-        main.synchronize()
+        main.synchronize()        # the next actions are in host memory
         if pending:
             read(pending.pop())
         pending.append((batch, ev, h))
@@ -352,9 +358,11 @@ def run_e2e(args, gdef, kern, root, dev, world, slot0, B):
         dt = float(tt.item())
     return {"value": B * world * args.steps / dt, "unit": "env-steps/s", "h2d_bytes_per_step": 8 * B,
             "d2h_bytes_per_step": (4 * P + 2 + 4 + 8) * B, "steps": args.steps,
-            "path": "public core.batch_step with a pinned host action buffer (H2D inside) + D2H of the next "
-                    "actions (critical path) and of rewards/flags/player (copy stream, read by the host one "
-                    "step later), same window as value (fresh init, W warm-up, K timed)"}
+            "path": "public core.batch_step: the step kernel reads the host agent's actions from pinned host "
+                    "memory and writes the next actions there (zero-copy over PCIe; BBK_ZERO_COPY=0 copies "
+                    "instead); rewards/flags/player D2H on a copy stream, read by the host one step later; "
+                    "same window as value (fresh init, W warm-up, K timed)",
+            "zero_copy": ZERO_COPY}
 
 
 def run_sweep(args, gdef, kern, dev, slot0):

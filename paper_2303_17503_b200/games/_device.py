@@ -122,6 +122,8 @@ class DeviceV:
         return arr
 
 
+# BBK_ZERO_COPY=0: copy pinned host action buffers to the device instead of reading them in place
+ZERO_COPY = __import__("os").environ.get("BBK_ZERO_COPY", "1") != "0"
 POOL_DEPTH = 2        # dead batches' buffer sets kept per (n, device, obs, stream)
 _CACHED = ("_cols", "_gostate")   # ctypes structs of fixed column pointers, valid with the buffers
 
@@ -251,6 +253,12 @@ class DeviceKernel:
         torch = _torch()
         if next_key is not None and next_actions is None:
             next_actions = torch.empty(v.n, dtype=torch.int64, device=v.device)
+        elif next_actions is not None:
+            ok_place = next_actions.device == v.device or (next_actions.device.type == "cpu" and next_actions.is_pinned())
+            if (next_actions.dtype != torch.int64 or tuple(next_actions.shape) != (v.n,) or not ok_place
+                    or not next_actions.is_contiguous()):
+                raise ShapeMismatch(f"next_actions must be a contiguous int64 [{v.n}] tensor on {v.device} "
+                                    "or in pinned host memory")
         if next_key is not None:
             v.next_actions = next_actions
             v.next_key = key_state(next_key)
@@ -266,10 +274,16 @@ class DeviceKernel:
         if isinstance(actions, torch.Tensor):
             a = actions
             if a.device != v.device or a.dtype != torch.int64:
-                # a pinned host int64 buffer is copied asynchronously on the launch stream (the step
-                # kernel is ordered after it; the caller must not rewrite the buffer before the
-                # step's results are read, as with any CUDA async copy)
                 pinned = a.device.type == "cpu" and a.dtype == torch.int64 and a.is_pinned()
+                if pinned and ZERO_COPY and a.dim() == 1 and a.is_contiguous():
+                    # zero-copy: page-locked host memory is device-addressable (UVA), so the step
+                    # kernel reads each slot's action over PCIe itself, prefetched with the slot's
+                    # state; the caller must not rewrite the buffer before the step's results are
+                    # read, as with any CUDA async copy
+                    if a.shape[0] != v.n:
+                        raise ShapeMismatch(f"expected {v.n} actions, got shape {tuple(a.shape)}")
+                    return a
+                # otherwise a pinned buffer is copied asynchronously on the launch stream
                 a = a.to(device=v.device, dtype=torch.int64, non_blocking=pinned)
         else:
             arr = np.ascontiguousarray(np.asarray(actions, dtype=np.int64))

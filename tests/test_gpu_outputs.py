@@ -29,3 +29,31 @@ def test_outputs_device_dlpack_and_wire(game):
         assert t.data_ptr() == d.data_ptr()      # zero copy
         assert wire[k].dtype == h.dtype and wire[k].shape == h.shape
         assert np.array_equal(wire[k], h), k
+
+
+@pytest.mark.parametrize("game", ["go_9x9", "go_19x19", "backgammon", "chess", "shogi", "othello"])
+def test_pinned_host_actions_zero_copy(game):
+    """batch_step on pinned host action buffers (read / written in place by the kernel, bench e2e)
+    gives the same trajectory as device actions, and recycled buffers never leak state."""
+    import torch
+
+    from paper_2303_17503_b200.agents import random_actions_device
+
+    n, root = 53, bb.RngKey(11)
+    from paper_2303_17503_b200.core import resolve
+
+    gdef = resolve(game)
+    ref = bb.batch_init(gdef, root.child(0), n)
+    zc = bb.batch_init(gdef, root.child(0), n)
+    acts = [torch.empty(n, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    acts[0].copy_(random_actions_device(zc, root.child(1)))
+    for t in range(40):
+        a = random_actions_device(ref, root.child(2 * t + 1))
+        ref = bb.batch_step(ref, a, root.child(2 * (t + 1)))
+        zc = bb.batch_step(zc, acts[t % 2], root.child(2 * (t + 1)), next_key=root.child(2 * t + 3),
+                           next_actions=acts[(t + 1) % 2])
+        torch.cuda.synchronize()
+        assert np.array_equal(acts[t % 2].numpy(), a.cpu().numpy()), t
+        assert np.array_equal(acts[(t + 1) % 2].numpy(), random_actions_device(ref, root.child(2 * t + 3)).cpu().numpy())
+        for k in ("legal_action_mask", "rewards", "terminated", "truncated", "current_player", "observation"):
+            assert np.array_equal(getattr(zc, k), getattr(ref, k)), (t, k)
