@@ -35,6 +35,46 @@ __device__ __constant__ int8_t KN_DR[8] = {2, 1, -1, -2, -2, -1, 1, 2};
 __device__ __constant__ int8_t KN_DF[8] = {1, 2, 2, 1, -1, -2, -2, -1};
 __device__ __constant__ int8_t DIR_DR[8] = {1, 1, 0, -1, -1, -1, 0, 1};
 __device__ __constant__ int8_t DIR_DF[8] = {0, 1, 1, 1, 0, -1, -1, -1};
+// square deltas of the knight jumps / king steps above (dr * 8 + df)
+__device__ __constant__ int8_t KN_DELTA[8] = {17, 10, -6, -15, -17, -10, 6, 15};
+__device__ __constant__ int8_t KG_DELTA[8] = {8, 9, 1, -7, -8, -9, -1, 7};
+// knight / king target sets per square (read through the read-only path: lanes index them divergently)
+__device__ const uint64_t KN_ATT[64] = {
+    0x0000000000020400ull, 0x0000000000050800ull, 0x00000000000A1100ull, 0x0000000000142200ull,
+    0x0000000000284400ull, 0x0000000000508800ull, 0x0000000000A01000ull, 0x0000000000402000ull,
+    0x0000000002040004ull, 0x0000000005080008ull, 0x000000000A110011ull, 0x0000000014220022ull,
+    0x0000000028440044ull, 0x0000000050880088ull, 0x00000000A0100010ull, 0x0000000040200020ull,
+    0x0000000204000402ull, 0x0000000508000805ull, 0x0000000A1100110Aull, 0x0000001422002214ull,
+    0x0000002844004428ull, 0x0000005088008850ull, 0x000000A0100010A0ull, 0x0000004020002040ull,
+    0x0000020400040200ull, 0x0000050800080500ull, 0x00000A1100110A00ull, 0x0000142200221400ull,
+    0x0000284400442800ull, 0x0000508800885000ull, 0x0000A0100010A000ull, 0x0000402000204000ull,
+    0x0002040004020000ull, 0x0005080008050000ull, 0x000A1100110A0000ull, 0x0014220022140000ull,
+    0x0028440044280000ull, 0x0050880088500000ull, 0x00A0100010A00000ull, 0x0040200020400000ull,
+    0x0204000402000000ull, 0x0508000805000000ull, 0x0A1100110A000000ull, 0x1422002214000000ull,
+    0x2844004428000000ull, 0x5088008850000000ull, 0xA0100010A0000000ull, 0x4020002040000000ull,
+    0x0400040200000000ull, 0x0800080500000000ull, 0x1100110A00000000ull, 0x2200221400000000ull,
+    0x4400442800000000ull, 0x8800885000000000ull, 0x100010A000000000ull, 0x2000204000000000ull,
+    0x0004020000000000ull, 0x0008050000000000ull, 0x00110A0000000000ull, 0x0022140000000000ull,
+    0x0044280000000000ull, 0x0088500000000000ull, 0x0010A00000000000ull, 0x0020400000000000ull,
+};
+__device__ const uint64_t KG_ATT[64] = {
+    0x0000000000000302ull, 0x0000000000000705ull, 0x0000000000000E0Aull, 0x0000000000001C14ull,
+    0x0000000000003828ull, 0x0000000000007050ull, 0x000000000000E0A0ull, 0x000000000000C040ull,
+    0x0000000000030203ull, 0x0000000000070507ull, 0x00000000000E0A0Eull, 0x00000000001C141Cull,
+    0x0000000000382838ull, 0x0000000000705070ull, 0x0000000000E0A0E0ull, 0x0000000000C040C0ull,
+    0x0000000003020300ull, 0x0000000007050700ull, 0x000000000E0A0E00ull, 0x000000001C141C00ull,
+    0x0000000038283800ull, 0x0000000070507000ull, 0x00000000E0A0E000ull, 0x00000000C040C000ull,
+    0x0000000302030000ull, 0x0000000705070000ull, 0x0000000E0A0E0000ull, 0x0000001C141C0000ull,
+    0x0000003828380000ull, 0x0000007050700000ull, 0x000000E0A0E00000ull, 0x000000C040C00000ull,
+    0x0000030203000000ull, 0x0000070507000000ull, 0x00000E0A0E000000ull, 0x00001C141C000000ull,
+    0x0000382838000000ull, 0x0000705070000000ull, 0x0000E0A0E0000000ull, 0x0000C040C0000000ull,
+    0x0003020300000000ull, 0x0007050700000000ull, 0x000E0A0E00000000ull, 0x001C141C00000000ull,
+    0x0038283800000000ull, 0x0070507000000000ull, 0x00E0A0E000000000ull, 0x00C040C000000000ull,
+    0x0302030000000000ull, 0x0705070000000000ull, 0x0E0A0E0000000000ull, 0x1C141C0000000000ull,
+    0x3828380000000000ull, 0x7050700000000000ull, 0xE0A0E00000000000ull, 0xC040C00000000000ull,
+    0x0203000000000000ull, 0x0507000000000000ull, 0x0A0E000000000000ull, 0x141C000000000000ull,
+    0x2838000000000000ull, 0x5070000000000000ull, 0xA0E0000000000000ull, 0x40C0000000000000ull,
+};
 
 struct WarpSmem {
     alignas(16) uint32_t mbits[A / 32];   // legal mask staged as bits (action a = bit a)
@@ -134,7 +174,6 @@ __device__ __forceinline__ int action_of(int fl, int from, int to, int promo) {
 // lanes then stride over the task list, so the (few, uneven) pieces do not
 // serialise the warp. Task = square | dir << 6 (dir 8 = whole piece).
 __device__ __constant__ int8_t FLIPD[8] = {4, 3, 2, 1, 0, 7, 6, 5};   // vertical flip of a queen direction
-__device__ __constant__ int8_t FLIPK[8] = {3, 2, 1, 0, 7, 6, 5, 4};   // vertical flip of a knight jump
 
 __device__ __forceinline__ void setm(uint32_t* m, int a) { atomicOr(&m[a >> 5], 1u << (a & 31)); }
 
@@ -185,9 +224,9 @@ __device__ __forceinline__ uint64_t task_attacks(const uint8_t* bd, uint16_t tk,
             rr += DIR_DR[d]; ff += DIR_DF[d];
         }
     } else if (t == N) {
-        for (int k = 0; k < 8; k++) { int rr = r + KN_DR[k], ff = f + KN_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+        a = __ldg(&KN_ATT[sq]);
     } else if (t == K) {
-        for (int k = 0; k < 8; k++) { int rr = r + DIR_DR[k], ff = f + DIR_DF[k]; if (on(rr, ff)) a |= 1ull << (rr * 8 + ff); }
+        a = __ldg(&KG_ATT[sq]);
     } else {   // pawn
         const int rr = by == 0 ? r + 1 : r - 1;
         if (on(rr, f - 1)) a |= 1ull << (rr * 8 + f - 1);
@@ -200,7 +239,7 @@ struct GenCtx {
     const uint8_t* bd;
     uint32_t* mask;   // bit per action
     int side, fl, ksq, ep;
-    uint64_t att, checkmask;
+    uint64_t att, checkmask, own;   // own: squares of the side to move
     const int8_t* pinsq;
     const uint64_t* pinray;
 };
@@ -213,13 +252,12 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
     const int from = (sq ^ c.fl) * 73;
     int cnt = 0;
     if (t == K) {
+        // a wrapped square sq + delta is never a king target of sq, so the set test is exact
+        const uint64_t m = __ldg(&KG_ATT[sq]) & ~c.own & ~c.att;
+#pragma unroll
         for (int k = 0; k < 8; k++) {
-            const int rr = r + DIR_DR[k], ff = f + DIR_DF[k];
-            if (!on(rr, ff)) continue;
-            const int to = rr * 8 + ff;
-            const uint8_t q = c.bd[to];
-            if ((q && color(q) == side) || ((c.att >> to) & 1ull)) continue;
-            setm(c.mask, from + (c.fl ? FLIPD[k] : k) * 7); cnt++;
+            const int to = sq + KG_DELTA[k];
+            if ((unsigned)to < 64u && ((m >> to) & 1ull)) { setm(c.mask, from + (c.fl ? (12 - k) & 7 : k) * 7); cnt++; }
         }
         return cnt;
     }
@@ -240,13 +278,11 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
         return cnt;
     }
     if (t == N) {
+        const uint64_t m = __ldg(&KN_ATT[sq]) & ~c.own & allow;
+#pragma unroll
         for (int k = 0; k < 8; k++) {
-            const int rr = r + KN_DR[k], ff = f + KN_DF[k];
-            if (!on(rr, ff)) continue;
-            const int to = rr * 8 + ff;
-            const uint8_t q = c.bd[to];
-            if ((q && color(q) == side) || !((allow >> to) & 1ull)) continue;
-            setm(c.mask, from + 56 + (c.fl ? FLIPK[k] : k)); cnt++;
+            const int to = sq + KN_DELTA[k];
+            if ((unsigned)to < 64u && ((m >> to) & 1ull)) { setm(c.mask, from + 56 + (c.fl ? (11 - k) & 7 : k)); cnt++; }
         }
         return cnt;
     }
@@ -367,7 +403,7 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
     asm volatile("cp.async.commit_group;");
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 56 registers, no spills
+__global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 56 registers, no spills
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
@@ -496,6 +532,11 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 5
         c.bd = S.bd; c.mask = S.mbits; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
         c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
         c.pinsq = S.pinsq; c.pinray = S.pinray;
+        {
+            const uint8_t q0 = S.bd[lane], q1 = S.bd[lane + 32];
+            c.own = (uint64_t)__ballot_sync(BBK_FULL, q0 && color(q0) == side) |
+                    ((uint64_t)__ballot_sync(BBK_FULL, q1 && color(q1) == side) << 32);
+        }
         bool ep_legal = false;
         int cnt = 0;
         for (int i = lane; i < n_own; i += 32) cnt += task_moves(c, S.task[0][i], ep_legal);
