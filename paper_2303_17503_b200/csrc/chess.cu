@@ -210,20 +210,23 @@ __device__ void build_tasks(const uint8_t* bd, int side, uint16_t (*task)[96], i
 }
 
 // Attack bits of one opponent task (our king `ksq` is transparent to sliders).
-__device__ __forceinline__ uint64_t task_attacks(const uint8_t* bd, uint16_t tk, int ksq) {
+__device__ __forceinline__ uint64_t task_attacks(const uint8_t* bd, uint16_t tk, uint64_t occ_nk) {
     const int sq = tk & 63, d = tk >> 6, r = sq >> 3, f = sq & 7;
-    const uint8_t pc = bd[sq];
-    const int t = type(pc), by = color(pc);
     uint64_t a = 0ull;
-    if (d < 8) {
-        int rr = r + DIR_DR[d], ff = f + DIR_DF[d];
+    if (d < 8) {   // walk the ray on the occupancy bitboard (our king transparent): no board reads
+        const int dr = DIR_DR[d], df = DIR_DF[d];
+        int rr = r + dr, ff = f + df;
         while (on(rr, ff)) {
             const int to = rr * 8 + ff;
             a |= 1ull << to;
-            if (bd[to] && to != ksq) break;
-            rr += DIR_DR[d]; ff += DIR_DF[d];
+            if ((occ_nk >> to) & 1ull) break;
+            rr += dr; ff += df;
         }
-    } else if (t == N) {
+        return a;
+    }
+    const uint8_t pc = bd[sq];
+    const int t = type(pc), by = color(pc);
+    if (t == N) {
         a = __ldg(&KN_ATT[sq]);
     } else if (t == K) {
         a = __ldg(&KG_ATT[sq]);
@@ -239,7 +242,7 @@ struct GenCtx {
     const uint8_t* bd;
     uint32_t* mask;   // bit per action
     int side, fl, ksq, ep;
-    uint64_t att, checkmask, own;   // own: squares of the side to move
+    uint64_t att, checkmask, own, occ;   // own: squares of the side to move; occ: all pieces
     const int8_t* pinsq;
     const uint64_t* pinray;
 };
@@ -266,14 +269,14 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
     for (int j = 0; j < 8; j++) if (c.pinsq[j] == sq) allow &= c.pinray[j];
     if (d < 8) {   // slider ray
         const int dm = (c.fl ? FLIPD[d] : d) * 7;
-        int rr = r + DIR_DR[d], ff = f + DIR_DF[d], k = 0;
+        const int dr = DIR_DR[d], df = DIR_DF[d];
+        int rr = r + dr, ff = f + df, k = 0;
         while (on(rr, ff)) {
             const int to = rr * 8 + ff;
-            const uint8_t q = c.bd[to];
-            if (q && color(q) == side) break;
+            if ((c.own >> to) & 1ull) break;
             if ((allow >> to) & 1ull) { setm(c.mask, from + dm + k); cnt++; }
-            if (q) break;
-            rr += DIR_DR[d]; ff += DIR_DF[d]; k++;
+            if ((c.occ >> to) & 1ull) break;
+            rr += dr; ff += df; k++;
         }
         return cnt;
     }
@@ -301,17 +304,16 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
         }
     };
     const int to1 = r1 * 8 + f;
-    if (!c.bd[to1]) {
+    if (!((c.occ >> to1) & 1ull)) {
         if ((allow >> to1) & 1ull) emit(to1, 0, 0 * 7 + 0);
         const int to2 = (r + 2 * dr) * 8 + f;
-        if (r == start && !c.bd[to2] && ((allow >> to2) & 1ull)) emit(to2, 0, 0 * 7 + 1);
+        if (r == start && !((c.occ >> to2) & 1ull) && ((allow >> to2) & 1ull)) emit(to2, 0, 0 * 7 + 1);
     }
     for (int df = -1; df <= 1; df += 2) {
         if (!on(r1, f + df)) continue;
         const int to = r1 * 8 + f + df;
-        const uint8_t q = c.bd[to];
         const int plane = (df < 0 ? 7 : 1) * 7;               // NW / NE, distance 1
-        if (q && color(q) != side) {
+        if (((c.occ & ~c.own) >> to) & 1ull) {
             if ((allow >> to) & 1ull) emit(to, df, plane);
         } else if (to == c.ep) {
             const int cap = side == 0 ? to - 8 : to + 8;
@@ -482,11 +484,19 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         const unsigned kb0 = __ballot_sync(BBK_FULL, S.bd[lane] == mk(side, K));
         const unsigned kb1 = __ballot_sync(BBK_FULL, S.bd[lane + 32] == mk(side, K));
         const int ksq = kb0 ? __ffs(kb0) - 1 : kb1 ? 32 + __ffs(kb1) - 1 : 0;
+        uint64_t own_bb, occ_bb;
+        {
+            const uint8_t q0 = S.bd[lane], q1 = S.bd[lane + 32];
+            own_bb = (uint64_t)__ballot_sync(BBK_FULL, q0 && color(q0) == side) |
+                     ((uint64_t)__ballot_sync(BBK_FULL, q1 && color(q1) == side) << 32);
+            occ_bb = (uint64_t)__ballot_sync(BBK_FULL, q0 != 0) | ((uint64_t)__ballot_sync(BBK_FULL, q1 != 0) << 32);
+        }
         int n_own, n_opp;
         build_tasks(S.bd, side, S.task, n_own, n_opp, lane);
         __syncwarp();
         uint64_t att_l = 0ull;
-        for (int i = lane; i < n_opp; i += 32) att_l |= task_attacks(S.bd, S.task[1][i], ksq);
+        const uint64_t occ_nk = occ_bb & ~(1ull << ksq);   // our king is transparent to sliders
+        for (int i = lane; i < n_opp; i += 32) att_l |= task_attacks(S.bd, S.task[1][i], occ_nk);
         const uint64_t att = warp_or64(att_l);
         const bool in_check = (att >> ksq) & 1ull;
         bool checker = false;
@@ -532,11 +542,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         c.bd = S.bd; c.mask = S.mbits; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
         c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
         c.pinsq = S.pinsq; c.pinray = S.pinray;
-        {
-            const uint8_t q0 = S.bd[lane], q1 = S.bd[lane + 32];
-            c.own = (uint64_t)__ballot_sync(BBK_FULL, q0 && color(q0) == side) |
-                    ((uint64_t)__ballot_sync(BBK_FULL, q1 && color(q1) == side) << 32);
-        }
+        c.own = own_bb; c.occ = occ_bb;
         bool ep_legal = false;
         int cnt = 0;
         for (int i = lane; i < n_own; i += 32) cnt += task_moves(c, S.task[0][i], ep_legal);
