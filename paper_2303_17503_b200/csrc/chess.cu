@@ -509,11 +509,12 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
             int own = -1;
             int8_t pin = -1;
             uint64_t pray = 0ull;
+            const int dr = DIR_DR[d], df = DIR_DF[d];
             while (on(rr, ff)) {
                 int s = rr * 8 + ff;
                 ray |= 1ull << s;
-                uint8_t pc = S.bd[s];
-                if (pc) {
+                if ((occ_bb >> s) & 1ull) {   // the board is read only at the (at most two) blockers
+                    const uint8_t pc = S.bd[s];
                     bool slider = color(pc) == opp && (type(pc) == Q || type(pc) == (diag ? B : R));
                     if (own < 0) {
                         if (color(pc) == side) own = s;
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
                         break;
                     }
                 }
-                rr += DIR_DR[d]; ff += DIR_DF[d];
+                rr += dr; ff += df;
             }
             S.pinsq[d] = pin;
             S.pinray[d] = pray;
