@@ -242,7 +242,7 @@ struct GenCtx {
     const uint8_t* bd;
     uint32_t* mask;   // bit per action
     int side, fl, ksq, ep;
-    uint64_t att, checkmask, own, occ;   // own: squares of the side to move; occ: all pieces
+    uint64_t att, checkmask, own, occ, pinned;   // own: side to move's squares; occ: all pieces
     const int8_t* pinsq;
     const uint64_t* pinray;
 };
@@ -266,7 +266,8 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
     }
     uint64_t allow = c.checkmask;
 #pragma unroll
-    for (int j = 0; j < 8; j++) if (c.pinsq[j] == sq) allow &= c.pinray[j];
+    if ((c.pinned >> sq) & 1ull)   // the 8 pin slots are read only for a pinned piece
+        for (int j = 0; j < 8; j++) if (c.pinsq[j] == sq) allow &= c.pinray[j];
     if (d < 8) {   // slider ray
         const int dm = (c.fl ? FLIPD[d] : d) * 7;
         const int dr = DIR_DR[d], df = DIR_DF[d];
@@ -538,11 +539,12 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         }
         const int nchecks = __popc(__ballot_sync(BBK_FULL, checker));
         const uint64_t blockall = warp_or64(block);
+        const uint64_t pinned_bb = warp_or64(lane < 8 && S.pinsq[lane] >= 0 ? 1ull << S.pinsq[lane] : 0ull);
         __syncwarp();
         GenCtx c;
         c.bd = S.bd; c.mask = S.mbits; c.side = side; c.fl = fl; c.ksq = ksq; c.att = att; c.ep = ep;
         c.checkmask = nchecks == 0 ? ~0ull : nchecks == 1 ? blockall : 0ull;
-        c.pinsq = S.pinsq; c.pinray = S.pinray;
+        c.pinsq = S.pinsq; c.pinray = S.pinray; c.pinned = pinned_bb;
         c.own = own_bb; c.occ = occ_bb;
         bool ep_legal = false;
         int cnt = 0;
