@@ -153,6 +153,9 @@ __device__ __forceinline__ int64_t warp_sample_bits(const uint32_t* bits, int nw
     return __shfl_sync(BBK_FULL, act, __ffs(who) - 1);
 }
 
+// kPadsZero: the caller guarantees that the bytes of the 16-byte chunks outside [0, A) are zero
+// (a zeroed staging buffer), so the edge chunks need no masking.
+template <bool kPadsZero = false>
 __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A, int count, uint64_t key,
                                                      int64_t slot) {
     if (count <= 0) return 0;
@@ -174,7 +177,7 @@ __device__ __forceinline__ int64_t warp_sample_bytes(const uint8_t* mask, int A,
     auto chunk_at = [&](int i) -> uint4 {
         uint4 v = w[i];
         const int b0 = 16 * i - head;
-        if (b0 < 0 || b0 + 16 > A) {
+        if (!kPadsZero && (b0 < 0 || b0 + 16 > A)) {
             v.x &= word_mask(b0); v.y &= word_mask(b0 + 4); v.z &= word_mask(b0 + 8); v.w &= word_mask(b0 + 12);
         }
         return v;

@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
         const bool truncated = !terminal && step >= p.max_steps;
         eps += (terminal || truncated) ? 1 : 0;
         if (p.out.next_actions) {   // fused agents.random_actions on the new mask (still in shared memory)
-            const int64_t a = warp_sample_bytes(mk, A, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
+            const int64_t a = warp_sample_bytes<true>(mk, A, (terminal || truncated) ? 0 : nlegal, p.out.next_key,
                                                 p.slot0 + b);
             if (lane == 0) p.out.next_actions[b] = a;
         }
