@@ -459,18 +459,16 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
             stm = (int)(misc & 0xFF); castle = (int)((misc >> 8) & 0xFF); ep = (int8_t)((misc >> 16) & 0xFF);
             halfmove = (int)((misc >> 24) & 0xFF);
             step = f_step + 1;
-            // past boards t = 1..7 from the prefetched packed copies
-            for (int t = 1; t < 8; t++) {
-                if (step - t >= 0) {
-                    const uint8_t byte = S.pf_past[t - 1][lane];
-                    S.past[t][2 * lane] = byte & 15;
-                    S.past[t][2 * lane + 1] = byte >> 4;
-                    if (lane == 0) S.prep[t] = (uint8_t)(S.pf_meta[(step - t) & (RING - 1)] >> 24);
-                } else {
-                    S.past[t][lane] = 0; S.past[t][lane + 32] = 0;
-                    if (lane == 0) S.prep[t] = 0;
-                }
+            // past boards t = 1..7 from the prefetched packed copies (two squares per byte): word w
+            // of the packed area is 8 squares of board t = w / 8 + 1, unpacked by two byte permutes
+            for (int w = lane; w < 7 * 8; w += 32) {
+                const int t = (w >> 3) + 1;
+                const uint32_t x = step - t >= 0 ? reinterpret_cast<const uint32_t*>(S.pf_past)[w] : 0u;
+                const uint32_t e = x & 0x0F0F0F0Fu, o = (x >> 4) & 0x0F0F0F0Fu;
+                reinterpret_cast<uint2*>(&S.past[1][0])[w] = make_uint2(__byte_perm(e, o, 0x5140), __byte_perm(e, o, 0x7362));
             }
+            if (lane >= 1 && lane < 8)
+                S.prep[lane] = step - lane >= 0 ? (uint8_t)(S.pf_meta[(step - lane) & (RING - 1)] >> 24) : (uint8_t)0;
             __syncwarp();
             if (lane == 0) apply_action(S.bd, stm, castle, ep, halfmove, f_act);
             stm = __shfl_sync(BBK_FULL, stm, 0); castle = __shfl_sync(BBK_FULL, castle, 0);
