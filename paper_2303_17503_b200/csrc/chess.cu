@@ -78,7 +78,7 @@ __device__ const uint64_t KG_ATT[64] = {
 
 struct WarpSmem {
     alignas(16) uint32_t mbits[A / 32];   // legal mask staged as bits (action a = bit a)
-    alignas(16) uint32_t bits[NF / 32 + 4];
+    alignas(16) uint32_t bits[(NF / 32 + 4 + 3) & ~3];   // zeroed as uint4
     alignas(16) uint8_t bd[64];
     alignas(16) uint8_t packed[32];
     alignas(16) uint8_t past[8][64];   // boards of history steps t = 0..7 (absolute squares)
@@ -599,8 +599,11 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
                 else bdark++;
             }
         }
-        heavy = warp_sum(heavy); minors = warp_sum(minors); knights = warp_sum(knights);
-        blight = warp_sum(blight); bdark = warp_sum(bdark);
+        {   // one reduction of the five counts (each <= 32) packed in 6-bit fields
+            const int sum = warp_sum(heavy | (minors << 6) | (knights << 12) | (blight << 18) | (bdark << 24));
+            heavy = sum & 63; minors = (sum >> 6) & 63; knights = (sum >> 12) & 63;
+            blight = (sum >> 18) & 63; bdark = (sum >> 24) & 63;
+        }
         const bool insufficient = heavy == 0 && (minors <= 1 || (knights == 0 && (blight == 0 || bdark == 0)));
         bool terminal = false;
         float rr0 = 0.0f, rr1 = 0.0f;
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         if (lane < 2) reinterpret_cast<uint4*>(hist + (step & (RING - 1)) * 32)[lane] =
             reinterpret_cast<const uint4*>(S.packed)[lane];
         if (lane == 0) hmeta[step & (RING - 1)] = meta_key | ((uint32_t)rep << 24);
-        S.past[0][lane] = S.bd[lane]; S.past[0][lane + 32] = S.bd[lane + 32];
+        reinterpret_cast<uint16_t*>(S.past[0])[lane] = reinterpret_cast<const uint16_t*>(S.bd)[lane];
         if (reset) {
             for (int t = 1; t < 8; t++) { S.past[t][lane] = 0; S.past[t][lane + 32] = 0; }
             if (lane < 8) S.prep[lane] = 0;
@@ -635,7 +638,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
             cur = nxt;
             pf_ready = true;
         }
-        for (int i = lane; i < NF / 32 + 4; i += 32) S.bits[i] = 0u;
+        for (int i = lane; i < (int)(sizeof(S.bits) / 16); i += 32) reinterpret_cast<uint4*>(S.bits)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         // ---- observation bitstream: square v (mover frame) owns bits [119 v, 119 v + 119)
         const int own_k = side ? 4 : 1, own_q = side ? 8 : 2, opp_k = side ? 1 : 4, opp_q = side ? 2 : 8;
@@ -703,7 +706,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
             m4[i] = make_uint4(spread4(v & 15u), spread4((v >> 4) & 15u), spread4((v >> 8) & 15u), spread4(v >> 12));
         }
         uint8_t* ob = p.out_s.board + b * 64;
-        ob[lane] = S.bd[lane]; ob[lane + 32] = S.bd[lane + 32];
+        reinterpret_cast<uint16_t*>(ob)[lane] = reinterpret_cast<const uint16_t*>(S.bd)[lane];
         if (lane == 0) {
             uint8_t* m = p.out_s.misc + b * 8;
             m[0] = (uint8_t)stm; m[1] = (uint8_t)castle; m[2] = (uint8_t)ep; m[3] = (uint8_t)halfmove;
