@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         int role, pass_count, step, hlen;
         uint64_t h, hx;
         uint32_t Bk = 0u, Wh = 0u;
+        int counts = -1;   // (black stones) | (white stones) << 16 of the new board once known
         bool terminal = false;
         float rr0 = 0.0f, rr1 = 0.0f;
         int nscan;
@@ -620,7 +621,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 }
                 const uint64_t h2 = h ^ zkey<N>(a, role) ^ warp_xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
-                const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
+                counts = warp_sum(__popc(Bk) | (__popc(Wh) << 16));
+                const int nbk = counts & 0xFFFF, nwh = counts >> 16;
                 if (lane == 0) {
                     hist[hlen] = h2;
                     bloom_add(gbloom, h2);
@@ -663,7 +665,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            const int nbk = warp_sum(__popc(Bk)), nwh = warp_sum(__popc(Wh));
+            if (counts < 0) counts = warp_sum(__popc(Bk) | (__popc(Wh) << 16));
+            const int nbk = counts & 0xFFFF, nwh = counts >> 16;
             legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, p.self_capture != 0, lane);
         }
         __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
