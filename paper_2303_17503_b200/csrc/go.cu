@@ -423,21 +423,38 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
 
 // One scalar column of board b per lane (lanes 0-9), loaded a board ahead so the
 // loads are in flight while the current board is processed; read back by shuffles.
-__device__ __forceinline__ uint64_t load_field(const StepParams& p, int64_t b, int lane) {
+// Branch-free: lane j's column base and element size are fixed for the launch (FieldRef,
+// built once), so each board's load is one aligned 8-byte read and a shift instead of a
+// 10-way divergent switch. Reading the aligned word around a 1/2/4-byte element stays inside
+// the column's allocation (allocations are at least 8-byte granular).
+struct FieldRef {
+    const char* base;
+    uint32_t lsz;     // log2 element size
+    uint64_t mask;    // 0 for lanes without a field
+};
+
+__device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
     switch (lane) {
-        case 0: return p.in.terminated[b];
-        case 1: return p.in.truncated[b];
-        case 2: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
-        case 3: return p.in_s.role_to_move[b];
-        case 4: return p.in_s.pass_count[b];
-        case 5: return (uint32_t)p.in.step_count[b];
-        case 6: return p.in_s.hash[b];
-        case 7: return p.in_s.hist_xor[b];
-        case 8: return (uint32_t)p.in_s.hist_len[b];
-        case 9: return (uint64_t)p.actions[b];
-        default: return 0ull;
+        case 0: return {reinterpret_cast<const char*>(p.in.terminated), 0u, 0xFFull};
+        case 1: return {reinterpret_cast<const char*>(p.in.truncated), 0u, 0xFFull};
+        case 2: return {reinterpret_cast<const char*>(p.in.player_to_role), 1u, 0xFFFFull};
+        case 3: return {reinterpret_cast<const char*>(p.in_s.role_to_move), 0u, 0xFFull};
+        case 4: return {reinterpret_cast<const char*>(p.in_s.pass_count), 0u, 0xFFull};
+        case 5: return {reinterpret_cast<const char*>(p.in.step_count), 2u, 0xFFFFFFFFull};
+        case 6: return {reinterpret_cast<const char*>(p.in_s.hash), 3u, ~0ull};
+        case 7: return {reinterpret_cast<const char*>(p.in_s.hist_xor), 3u, ~0ull};
+        case 8: return {reinterpret_cast<const char*>(p.in_s.hist_len), 2u, 0xFFFFFFFFull};
+        case 9: return {reinterpret_cast<const char*>(p.actions), 3u, ~0ull};
+        default: return {reinterpret_cast<const char*>(p.in.terminated), 0u, 0ull};
     }
 }
+
+__device__ __forceinline__ uint64_t load_field(const FieldRef& f, int64_t b) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(f.base) + ((uintptr_t)b << f.lsz);
+    const uint64_t w = *reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
+    return (w >> (8u * (uint32_t)(a & 7u))) & f.mask;
+}
+
 
 template <int N>
 __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
@@ -471,7 +488,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     uint16_t* lab_pf = pat_pf + PS;
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
     const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-    uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(p, b0, lane) : 0ull;
+    const FieldRef fref = field_ref(p, lane);
+    uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(fref, b0) : 0ull;
     bool pat_ready = false;
 
     for (int64_t b = b0; b < p.n; b += nwarps) {
@@ -713,7 +731,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         pat_ready = false;
         if (!p.force_reset && b + nwarps < p.n) {   // issue the next board's loads now
             const int64_t nb = b + nwarps;
-            pf = load_field(p, nb, lane);
+            pf = load_field(fref, nb);
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
             const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
             const char* lsrc = reinterpret_cast<const char*>(p.in_s.lab + nb * (int64_t)PS);
