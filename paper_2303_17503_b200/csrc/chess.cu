@@ -358,14 +358,15 @@ __device__ void apply_action(uint8_t* bd, int& stm, int& castle, int& ep, int& h
 }
 
 // One scalar field of board b per lane (lanes 0-4), loaded a board ahead.
-__device__ __forceinline__ uint64_t load_field(const Params& p, int64_t b, int lane) {
+__device__ __forceinline__ FieldRef field_ref(const Params& p, int lane) {
     switch (lane) {
-        case 0: return (uint32_t)p.in.terminated[b] | ((uint32_t)p.in.truncated[b] << 8);
-        case 1: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
-        case 2: return *reinterpret_cast<const uint64_t*>(p.in_s.misc + b * 8);
-        case 3: return (uint32_t)p.in.step_count[b];
-        case 4: return (uint64_t)p.actions[b];
-        default: return 0ull;
+        case 0: return field_of(p.in.terminated, 0u);
+        case 1: return field_of(p.in.player_to_role, 1u);
+        case 2: return field_of(p.in_s.misc, 3u);
+        case 3: return field_of(p.in.step_count, 2u);
+        case 4: return field_of(p.actions, 3u);
+        case 5: return field_of(p.in.truncated, 0u);
+        default: return no_field();
     }
 }
 
@@ -421,15 +422,16 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
     const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     uint64_t cur = 0ull;   // this board's scalar fields (lane j holds field j)
     bool pf_ready = false;
+    const FieldRef fref = field_ref(p, lane_id());
     for (int64_t b = b0; b < p.n; b += nwarps) {
         if (!p.force_reset && !pf_ready) {   // first board of the warp: fetch synchronously
-            cur = load_field(p, b, lane);
+            cur = load_field(fref, b);
             issue_prefetch(S, p, b, cur, lane);
         }
         // the next board's scalars are in flight while this board is processed
         const int64_t nb = b + nwarps;
-        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(p, nb, lane) : 0ull;
-        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0);
+        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(fref, nb) : 0ull;
+        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0) | (__shfl_sync(BBK_FULL, (uint32_t)cur, 5) << 8);
         const bool reset = p.force_reset || (f_term & 0xFFFFu) != 0u;
         if (!p.force_reset) asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();

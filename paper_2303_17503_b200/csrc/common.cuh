@@ -116,6 +116,29 @@ __device__ __forceinline__ uint32_t chunk_count_bytes(uint4 v) {
 // 4 bits -> 4 bytes of 0 / 1 (bit k -> byte k)
 __device__ __forceinline__ uint32_t spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
 
+// Next-board scalar columns, one per lane (lane j holds field j, read back by shuffles). Lane j's
+// column base and element size are fixed for the launch, so each board's load is one aligned
+// 8-byte read and a shift instead of a divergent switch over the lanes. Reading the aligned word
+// around a 1/2/4-byte element stays inside the column's allocation (allocations are at least
+// 8-byte granular); lanes without a field get mask 0.
+struct FieldRef {
+    uint64_t v;   // column base | log2(element size) << 58 | no-field flag << 61 (one register pair)
+};
+
+__device__ __forceinline__ FieldRef field_of(const void* base, uint32_t lsz) {
+    return {reinterpret_cast<uint64_t>(base) | ((uint64_t)lsz << 58)};
+}
+__device__ __forceinline__ FieldRef no_field() { return {1ull << 61}; }
+
+__device__ __forceinline__ uint64_t load_field(FieldRef f, int64_t b) {
+    if (f.v >> 61) return 0ull;
+    const uint32_t lsz = (uint32_t)(f.v >> 58) & 3u;
+    const uint64_t a = (f.v & ((1ull << 58) - 1ull)) + ((uint64_t)b << lsz);
+    const uint64_t w = *reinterpret_cast<const uint64_t*>(a & ~7ull);
+    const uint64_t x = w >> (8u * (uint32_t)(a & 7u));
+    return lsz == 3u ? x : x & ((1ull << (8u << lsz)) - 1ull);
+}
+
 // agents.random_actions for ONE slot whose legal mask is staged as bits (action a = bit a of
 // bits[a / 32], nwords words): lanes count contiguous word ranges, scan, and the lane holding
 // the d-th set bit resolves it; d = child(key, slot) % count, 0 when count == 0.

@@ -423,37 +423,42 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
 
 // One scalar column of board b per lane (lanes 0-9), loaded a board ahead so the
 // loads are in flight while the current board is processed; read back by shuffles.
-// Branch-free: lane j's column base and element size are fixed for the launch (FieldRef,
-// built once), so each board's load is one aligned 8-byte read and a shift instead of a
-// 10-way divergent switch. Reading the aligned word around a 1/2/4-byte element stays inside
-// the column's allocation (allocations are at least 8-byte granular).
-struct FieldRef {
+// Go keeps the decoded form of the field reference in registers (it has register headroom; the
+// packed FieldRef of common.cuh is for the register-capped chess / shogi kernels).
+struct FieldRefWide {
     const char* base;
-    uint32_t lsz;     // log2 element size
-    uint64_t mask;    // 0 for lanes without a field
+    uint32_t lsz;
+    uint64_t mask;
 };
-
-__device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
-    switch (lane) {
-        case 0: return {reinterpret_cast<const char*>(p.in.terminated), 0u, 0xFFull};
-        case 1: return {reinterpret_cast<const char*>(p.in.truncated), 0u, 0xFFull};
-        case 2: return {reinterpret_cast<const char*>(p.in.player_to_role), 1u, 0xFFFFull};
-        case 3: return {reinterpret_cast<const char*>(p.in_s.role_to_move), 0u, 0xFFull};
-        case 4: return {reinterpret_cast<const char*>(p.in_s.pass_count), 0u, 0xFFull};
-        case 5: return {reinterpret_cast<const char*>(p.in.step_count), 2u, 0xFFFFFFFFull};
-        case 6: return {reinterpret_cast<const char*>(p.in_s.hash), 3u, ~0ull};
-        case 7: return {reinterpret_cast<const char*>(p.in_s.hist_xor), 3u, ~0ull};
-        case 8: return {reinterpret_cast<const char*>(p.in_s.hist_len), 2u, 0xFFFFFFFFull};
-        case 9: return {reinterpret_cast<const char*>(p.actions), 3u, ~0ull};
-        default: return {reinterpret_cast<const char*>(p.in.terminated), 0u, 0ull};
-    }
+// lanes without a field read (and mask off) the first byte of `any`, a valid column
+__device__ __forceinline__ FieldRefWide widen(FieldRef f, const void* any) {
+    const uint32_t lsz = (uint32_t)(f.v >> 58) & 3u;
+    if (f.v >> 61) return {reinterpret_cast<const char*>(any), 0u, 0ull};
+    return {reinterpret_cast<const char*>(f.v & ((1ull << 58) - 1ull)), lsz,
+            lsz == 3u ? ~0ull : (1ull << (8u << lsz)) - 1ull};
 }
-
-__device__ __forceinline__ uint64_t load_field(const FieldRef& f, int64_t b) {
+__device__ __forceinline__ uint64_t load_field(const FieldRefWide& f, int64_t b) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(f.base) + ((uintptr_t)b << f.lsz);
     const uint64_t w = *reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
     return (w >> (8u * (uint32_t)(a & 7u))) & f.mask;
 }
+
+__device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
+    switch (lane) {
+        case 0: return field_of(p.in.terminated, 0u);
+        case 1: return field_of(p.in.truncated, 0u);
+        case 2: return field_of(p.in.player_to_role, 1u);
+        case 3: return field_of(p.in_s.role_to_move, 0u);
+        case 4: return field_of(p.in_s.pass_count, 0u);
+        case 5: return field_of(p.in.step_count, 2u);
+        case 6: return field_of(p.in_s.hash, 3u);
+        case 7: return field_of(p.in_s.hist_xor, 3u);
+        case 8: return field_of(p.in_s.hist_len, 2u);
+        case 9: return field_of(p.actions, 3u);
+        default: return no_field();
+    }
+}
+
 
 
 template <int N>
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     uint16_t* lab_pf = pat_pf + PS;
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
     const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const FieldRef fref = field_ref(p, lane);
+    const FieldRefWide fref = widen(field_ref(p, lane), p.in.terminated);
     uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(fref, b0) : 0ull;
     bool pat_ready = false;
 

@@ -286,13 +286,14 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
 }
 
 // One scalar field of board b per lane (lanes 0-3), loaded a board ahead.
-__device__ __forceinline__ uint64_t load_field(const Params& p, int64_t b, int lane) {
+__device__ __forceinline__ FieldRef field_ref(const Params& p, int lane) {
     switch (lane) {
-        case 0: return (uint32_t)p.in.terminated[b] | ((uint32_t)p.in.truncated[b] << 8);
-        case 1: return *reinterpret_cast<const uint16_t*>(p.in.player_to_role + 2 * b);
-        case 2: return (uint32_t)p.in.step_count[b];
-        case 3: return (uint64_t)p.actions[b];
-        default: return 0ull;
+        case 0: return field_of(p.in.terminated, 0u);
+        case 1: return field_of(p.in.player_to_role, 1u);
+        case 2: return field_of(p.in.step_count, 2u);
+        case 3: return field_of(p.actions, 3u);
+        case 4: return field_of(p.in.truncated, 0u);
+        default: return no_field();
     }
 }
 
@@ -332,14 +333,15 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
     const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     uint64_t cur = 0ull;   // this board's scalar fields (lane j holds field j)
     bool pf_ready = false;
+    const FieldRef fref = field_ref(p, lane_id());
     for (int64_t b = b0; b < p.n; b += nwarps) {
         if (!p.force_reset && !pf_ready) {   // first board of the warp: fetch synchronously
-            cur = load_field(p, b, lane);
+            cur = load_field(fref, b);
             issue_prefetch(S, p, b, lane);
         }
         const int64_t nb = b + nwarps;   // the next board's scalars are in flight meanwhile
-        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(p, nb, lane) : 0ull;
-        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0);
+        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(fref, nb) : 0ull;
+        const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0) | (__shfl_sync(BBK_FULL, (uint32_t)cur, 4) << 8);
         const bool reset = p.force_reset || (f_term & 0xFFFFu) != 0u;
         if (!p.force_reset) asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
