@@ -587,6 +587,13 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         }
         reps = warp_sum(reps);
         const int rep = reps > 2 ? 2 : reps;
+        __syncwarp();   // the prefetch area (board, past boards, ring meta) is free now: issue the next board's state
+        pf_ready = false;
+        if (!p.force_reset && nb < p.n) {
+            issue_prefetch(S, p, nb, nxt, lane);
+            cur = nxt;
+            pf_ready = true;
+        }
         // ---- insufficient material (oracle insufficient())
         int minors = 0, heavy = 0, knights = 0, blight = 0, bdark = 0;
         for (int s = lane; s < 64; s += 32) {
@@ -633,13 +640,6 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
             if (lane < 8) S.prep[lane] = 0;
         }
         if (lane == 0) S.prep[0] = (uint8_t)rep;
-        __syncwarp();   // the prefetch area is free now: issue the next board's state
-        pf_ready = false;
-        if (!p.force_reset && nb < p.n) {
-            issue_prefetch(S, p, nb, nxt, lane);
-            cur = nxt;
-            pf_ready = true;
-        }
         for (int i = lane; i < (int)(sizeof(S.bits) / 16); i += 32) reinterpret_cast<uint4*>(S.bits)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         // ---- observation bitstream: square v (mover frame) owns bits [119 v, 119 v + 119)
