@@ -91,6 +91,8 @@ gpu__time_duration.sum`): the step kernel is the only kernel in the timed loop.
         src = os.path.join(OUT, f"bench_{g}.json")
         if os.path.exists(src):
             shutil.copy(src, os.path.join(dst, f"bench_{g}.json"))
+        src = os.path.join(dst, f"bench_{g}.json")   # a pass run with SMALL=0 keeps the previous lines
+        if os.path.exists(src):
             d = line(src)
             small.append(f"| {g} | {d['value'] / 1e6:,.1f} M | {d['roofline']['frac']:.3f} | "
                          f"{d['e2e']['value'] / 1e6:,.1f} M | {d['roofline']['bytes_per_env_step']:,} |")
