@@ -647,12 +647,24 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         const uint32_t cbits = ((uint32_t)side << 0) | ((uint32_t)((castle & own_k) != 0) << 2) |
                                ((uint32_t)((castle & own_q) != 0) << 3) | ((uint32_t)((castle & opp_k) != 0) << 4) |
                                ((uint32_t)((castle & opp_q) != 0) << 5);   // planes 112.. relative
+        // square-independent planes, once per board: repetition planes 14 t + 12 / 13 and
+        // 112.. colour, [113 count], castling x4, [118 count]
+        uint64_t clo = 0ull, chi = (uint64_t)cbits << (112 - 64);
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            const int base = 14 * t;
+            const uint8_t rp = S.prep[t];
+            const uint64_t r1 = rp >= 1 ? 1ull : 0ull, r2 = rp >= 2 ? 1ull : 0ull;
+            if (base + 13 < 64) clo |= (r1 << (base + 12)) | (r2 << (base + 13));
+            else if (base + 12 >= 64) chi |= (r1 << (base + 12 - 64)) | (r2 << (base + 13 - 64));
+            else { clo |= r1 << (base + 12); chi |= r2 << (base + 13 - 64); }
+        }
 #pragma unroll
         for (int pass = 0; pass < 2; pass++) {
             const int v = 2 * lane + pass;
             const int sabs = v ^ fl;
             // 119-bit pattern of square v (bit k = plane k) in two registers
-            uint64_t plo = 0ull, phi = 0ull;
+            uint64_t plo = clo, phi = chi;
 #pragma unroll
             for (int t = 0; t < 8; t++) {
                 const uint8_t pc = S.past[t][sabs];
@@ -662,14 +674,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
                     plo |= bit < 64 ? 1ull << bit : 0ull;
                     phi |= bit >= 64 ? 1ull << (bit - 64) : 0ull;
                 }
-                const uint8_t rp = S.prep[t];
-                const uint64_t r1 = rp >= 1 ? 1ull : 0ull, r2 = rp >= 2 ? 1ull : 0ull;
-                if (base + 13 < 64) plo |= (r1 << (base + 12)) | (r2 << (base + 13));
-                else if (base + 12 >= 64) phi |= (r1 << (base + 12 - 64)) | (r2 << (base + 13 - 64));
-                else { plo |= r1 << (base + 12); phi |= r2 << (base + 13 - 64); }
             }
-            // planes 112.. : colour, [113 count], castling x4, [118 count]
-            phi |= (uint64_t)cbits << (112 - 64);
             const uint32_t w[4] = {(uint32_t)plo, (uint32_t)(plo >> 32), (uint32_t)phi, (uint32_t)(phi >> 32)};
             // OR the 119-bit pattern into the stream at bit offset 119 v
             const int off = 119 * v, wi = off >> 5, sh = off & 31;
