@@ -80,12 +80,18 @@ struct WarpSmem {
     int32_t roff[33];
 };
 
-// zobrist key of (cell, colour) (go.py:20-25): mix64(0x60D00D60C0FFEE00 + N + 2*cell + colour),
-// computed in registers: with shared memory taking most of the unified L1, a table lookup
-// would be an L2 round trip; mix64 is ~15 ALU ops.
+// zobrist key of (cell, colour) (go.py:20-25): mix64(0x60D00D60C0FFEE00 + N + 2*cell + colour).
+// Boards up to 13x13 read it from a table filled once per device (launch_step) through the
+// read-only path -- one L1 load instead of a chain of ~15 dependent 64-bit multiply / shift ops
+// (go_9x9 +6.7 %); 15x15+ compute it in registers (their shared memory leaves little L1, and the
+// table lost 1.2 % at 19x19).
+template <int N>
+__device__ uint64_t g_zob[2 * N * N];
+
 template <int N>
 __device__ __forceinline__ uint64_t zkey(int cell, int colour) {
-    return mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)cell + (uint64_t)colour);
+    if constexpr (N <= 13) return __ldg(&g_zob<N>[2 * cell + colour]);
+    else return mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)cell + (uint64_t)colour);
 }
 
 template <int N>
@@ -833,15 +839,30 @@ static int num_sms() {
 template <int N>
 static int launch_step(const StepParams& p, cudaStream_t stream) {
     const size_t smem = sizeof(BlockSmem<N>);
-    static bool configured = false;
-    if (!configured) {
+    // per device, once: shared-memory opt-in, occupancy, zobrist table (synchronous copy, so an
+    // init launch -- always eager, before any capture -- leaves it ready for every later launch)
+    constexpr int kMaxDev = 64;
+    static int per_sm_dev[kMaxDev] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return (int)cudaErrorInvalidDevice;
+    if (!per_sm_dev[dev]) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(stream, &cs);
+        if (cs != cudaStreamCaptureStatusNone) return (int)cudaErrorStreamCaptureUnsupported;
         cudaFuncSetAttribute(step_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+        static uint64_t zob[2 * N * N];
+        for (int c = 0; c < N * N; c++)
+            for (int col = 0; col < 2; col++)
+                zob[2 * c + col] = mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)c + (uint64_t)col);
+        cudaError_t e = cudaMemcpyToSymbol(g_zob<N>, zob, sizeof(zob));
+        if (e != cudaSuccess) return (int)e;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<N>, kWarps * 32, smem);
+        per_sm_dev[dev] = per_sm < 1 ? 1 : per_sm;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<N>, kWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = per_sm_dev[dev];
     int64_t need = (p.n + kWarps - 1) / kWarps;
     int64_t grid = (int64_t)num_sms() * per_sm;
     if (grid > need) grid = need;
