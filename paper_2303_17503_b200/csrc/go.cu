@@ -546,29 +546,50 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             role = (int)f_role; pass_count = (int)f_pass;
             step = (int)f_step;
             h = f_hash; hx = f_hx; hlen = (int)f_hlen;
+            // copy pat / lab in; boards up to 13x13 take each 8-point chunk's current stones (bits 0 / 1
+            // of every u16) on the way as one byte of flat black / white bitmaps, from which each lane
+            // then cuts its row with one funnel shift (no per-point pass over the pattern; go_9x9 +1.9 %)
+            uint8_t* FB = reinterpret_cast<uint8_t*>(S.rX);   // free until legal_rows
+            uint8_t* FW = reinterpret_cast<uint8_t*>(S.rY);
+            auto take = [&](int i, uint4 v) {
+                reinterpret_cast<uint4*>(S.pat)[i] = v;
+                if constexpr (N > 13) return;   // 15x15+: rows from the pattern (below), measured faster
+                FB[i] = (uint8_t)((v.x & 1u) | ((v.x >> 15) & 2u) | ((v.y & 1u) << 2) | ((v.y >> 13) & 8u) |
+                                  ((v.z & 1u) << 4) | ((v.z >> 11) & 32u) | ((v.w & 1u) << 6) | ((v.w >> 9) & 128u));
+                FW[i] = (uint8_t)(((v.x >> 1) & 1u) | ((v.x >> 16) & 2u) | ((v.y << 1) & 4u) | ((v.y >> 14) & 8u) |
+                                  ((v.z << 3) & 16u) | ((v.z >> 12) & 32u) | ((v.w << 5) & 64u) | ((v.w >> 10) & 128u));
+            };
             if (pat_ready) {   // prefetched during the previous board
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
                 for (int i = lane; i < PS / 8; i += 32) {
-                    reinterpret_cast<uint4*>(S.pat)[i] = reinterpret_cast<const uint4*>(pat_pf)[i];
+                    take(i, reinterpret_cast<const uint4*>(pat_pf)[i]);
                     reinterpret_cast<uint4*>(lab)[i] = reinterpret_cast<const uint4*>(lab_pf)[i];
                 }
             } else {
                 const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
                 const uint4* lsrc = reinterpret_cast<const uint4*>(p.in_s.lab + b * (int64_t)PS);
                 for (int i = lane; i < PS / 8; i += 32) {
-                    reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+                    take(i, src[i]);
                     reinterpret_cast<uint4*>(lab)[i] = lsrc[i];
                 }
             }
             __syncwarp();
-            if (lane < N) {
+            if constexpr (N > 13) {
+                if (lane < N) {
 #pragma unroll 4
-                for (int col = 0; col < N; col++) {
-                    uint32_t v = S.pat[lane * N + col];
-                    Bk |= (v & 1u) << col;
-                    Wh |= ((v >> 1) & 1u) << col;
+                    for (int col = 0; col < N; col++) {
+                        uint32_t v = S.pat[lane * N + col];
+                        Bk |= (v & 1u) << col;
+                        Wh |= ((v >> 1) & 1u) << col;
+                    }
                 }
+            } else if (lane < N) {
+                const int q = lane * N, w = q >> 5, sh = q & 31;
+                const uint32_t* fb = reinterpret_cast<const uint32_t*>(FB);
+                const uint32_t* fw = reinterpret_cast<const uint32_t*>(FW);
+                Bk = __funnelshift_r(fb[w], fb[w + 1], sh) & ROW;
+                Wh = __funnelshift_r(fw[w], fw[w + 1], sh) & ROW;
             }
             const int a = (int)f_act;
             step += 1;
