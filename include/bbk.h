@@ -140,6 +140,14 @@ typedef struct bbk_chess_state {
 
 int bbk_chess_init(const bbk_cols* out, const bbk_chess_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
                    const uint64_t* slot_keys, int32_t max_steps, void* stream);
+/* Start slots from given positions (a reset with the position instead of the initial one; history
+ * empty, step_count 0, player_to_role from the slot key as in init). boards [n,64] piece codes,
+ * misc [n,8] = stm, castling bits, en-passant square (int8, -1 none), half-move clock. No reference
+ * interface (chess has no reference engine): the device twin of oracle/orc_chess.c orc_chess_set_fen,
+ * used by the device perft / rule-position tests. */
+int bbk_chess_load(const bbk_cols* out, const bbk_chess_state* out_s, const uint8_t* boards, const uint8_t* misc,
+                   int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys, int32_t max_steps,
+                   void* stream);
 int bbk_chess_step(const bbk_cols* in, const bbk_chess_state* in_s, const bbk_cols* out, const bbk_chess_state* out_s,
                    const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
                    int32_t max_steps, void* stream);
@@ -162,6 +170,11 @@ typedef struct bbk_shogi_state {
 
 int bbk_shogi_init(const bbk_cols* out, const bbk_shogi_state* out_s, int64_t n, int64_t slot0, uint64_t key_state,
                    const uint64_t* slot_keys, int32_t max_steps, void* stream);
+/* As bbk_chess_load: boards [n,96] absolute codes (owner << 4 | type, squares r*9+c), misc [n,16] =
+ * hands [2][7] (FU KY KE GI KI KA HI), side to move. Twin of oracle orc_shogi_set_sfen. */
+int bbk_shogi_load(const bbk_cols* out, const bbk_shogi_state* out_s, const uint8_t* boards, const uint8_t* misc,
+                   int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys, int32_t max_steps,
+                   void* stream);
 int bbk_shogi_step(const bbk_cols* in, const bbk_shogi_state* in_s, const bbk_cols* out, const bbk_shogi_state* out_s,
                    const int64_t* actions, int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
                    int32_t max_steps, void* stream);

@@ -107,6 +107,7 @@ def _declare(L):
     sig("bbk_latch_finished", [P, P, P, P, C.c_int, I64, P, P, P, P, P])
     for g, S in (("chess", ChessState), ("shogi", ShogiState)):
         sig(f"bbk_{g}_init", [ptr(Cols), ptr(S), I64, I64, U64, P, I32, P])
+        sig(f"bbk_{g}_load", [ptr(Cols), ptr(S), P, P, I64, I64, U64, P, I32, P])
         sig(f"bbk_{g}_step", [ptr(Cols), ptr(S), ptr(Cols), ptr(S), P, I64, I64, U64, P, I32, P])
         sig(f"bbk_{g}_observe", [ptr(S), P, P, P, I64, P])
     sig("bbk_fingerprint_stride", [C.c_int, C.c_int])

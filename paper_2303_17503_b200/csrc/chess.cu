@@ -101,6 +101,8 @@ struct Params {
     uint64_t key;
     int32_t max_steps;
     int force_reset;
+    const uint8_t* load_board;   // kLoad: positions to start from, [n, 64] / [n, 8] (stm, castle, ep, half-move)
+    const uint8_t* load_misc;
 };
 
 __device__ __forceinline__ bool on(int r, int f) { return (unsigned)r < 8u && (unsigned)f < 8u; }
@@ -407,6 +409,10 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
     asm volatile("cp.async.commit_group;");
 }
 
+// kLoad: a reset that starts from p.load_board / p.load_misc instead of the initial position
+// (bbk_chess_load, the device twin of the oracle's orc_chess_set_fen test hook); a separate
+// instantiation so the hot kernel's code is unchanged.
+template <bool kLoad>
 __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 56 registers, no spills
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
@@ -443,14 +449,22 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         if (reset) {
             int c = (int)(child(k, 0) % 2ull);
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
-            constexpr uint32_t back = 0x42365324u;   // R N B Q K B N R, nibble f = file f
-            for (int s = lane; s < 64; s += 32) {
-                int r = s >> 3, f = s & 7;
-                const int bk = (int)((back >> (4 * f)) & 15u);
-                uint8_t v = r == 0 ? mk(0, bk) : r == 1 ? mk(0, P) : r == 6 ? mk(1, P) : r == 7 ? mk(1, bk) : 0;
-                S.bd[s] = v;
+            if (kLoad) {
+                S.bd[lane] = p.load_board[b * 64 + lane];
+                S.bd[lane + 32] = p.load_board[b * 64 + lane + 32];
+                const uint8_t* lm = p.load_misc + b * 8;
+                stm = lm[0] & 1; castle = lm[1] & 15; ep = (int8_t)lm[2]; halfmove = lm[3];
+            } else {
+                constexpr uint32_t back = 0x42365324u;   // R N B Q K B N R, nibble f = file f
+                for (int s = lane; s < 64; s += 32) {
+                    int r = s >> 3, f = s & 7;
+                    const int bk = (int)((back >> (4 * f)) & 15u);
+                    uint8_t v = r == 0 ? mk(0, bk) : r == 1 ? mk(0, P) : r == 6 ? mk(1, P) : r == 7 ? mk(1, bk) : 0;
+                    S.bd[s] = v;
+                }
+                stm = 0; castle = 15; ep = -1; halfmove = 0;
             }
-            stm = 0; castle = 15; ep = -1; halfmove = 0; step = 0;
+            step = 0;
         } else {
             const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)cur, 1);
             const uint64_t misc = shfl64(cur, 2);
@@ -771,8 +785,12 @@ __global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, co
 }
 
 static int launch(const Params& p, cudaStream_t s) {
-    const int64_t grid = persistent_grid(step_kernel, kWarps * 32, 0, (p.n + kWarps - 1) / kWarps);
-    step_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(p);
+    const int64_t need = (p.n + kWarps - 1) / kWarps;
+    if (p.load_board) {
+        step_kernel<true><<<(unsigned)persistent_grid(step_kernel<true>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+    } else {
+        step_kernel<false><<<(unsigned)persistent_grid(step_kernel<false>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+    }
     return (int)cudaGetLastError();
 }
 
@@ -786,6 +804,17 @@ int bbk_chess_init(const bbk_cols* out, const bbk_chess_state* out_s, int64_t n,
     chess::Params p{};
     p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
     p.max_steps = max_steps; p.force_reset = 1;
+    return chess::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_chess_load(const bbk_cols* out, const bbk_chess_state* out_s, const uint8_t* boards, const uint8_t* misc,
+                   int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys, int32_t max_steps,
+                   void* stream) {
+    if (n <= 0) return 0;
+    if (!boards || !misc) return (int)cudaErrorInvalidValue;
+    chess::Params p{};
+    p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.force_reset = 1; p.load_board = boards; p.load_misc = misc;
     return chess::launch(p, (cudaStream_t)stream);
 }
 

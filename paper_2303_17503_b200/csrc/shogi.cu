@@ -76,6 +76,8 @@ struct Params {
     uint64_t key;
     int32_t max_steps;
     int force_reset;
+    const uint8_t* load_board;   // kLoad: positions to start from, [n, 96] absolute codes / [n, 16] hands + stm
+    const uint8_t* load_misc;
 };
 
 struct M81 {   // 81-bit square set
@@ -316,6 +318,10 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
     asm volatile("cp.async.commit_group;");
 }
 
+// kLoad: a reset that starts from p.load_board / p.load_misc instead of the initial position
+// (bbk_shogi_load, the device twin of the oracle's orc_shogi_set_sfen test hook); a separate
+// instantiation so the hot kernel's code is unchanged.
+template <bool kLoad>
 __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 64 registers: 8 CTAs per SM
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
@@ -353,23 +359,30 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
             int c = (int)(child(k, 0) % 2ull);
             p2r0 = (int8_t)c; p2r1 = (int8_t)(1 - c);
             // lnsgkgsnl/1r5b1/ppppppppp/9/9/9/PPPPPPPPP/1B5R1/LNSGKGSNL (White = owner 1 at the top)
-            constexpr uint64_t back = 0x234585432ull;   // KY KE GI KI OU KI GI KE KY, nibble c = file c
-            for (int s = lane; s < 96; s += 32) {
-                uint8_t v = 0;
-                if (s < 81) {
-                    int r = s / 9, cc = s - 9 * r;
-                    const uint8_t bk = (uint8_t)((back >> (4 * cc)) & 15u);
-                    if (r == 0) v = (uint8_t)(16 | bk);
-                    else if (r == 1) v = cc == 1 ? (uint8_t)(16 | HI) : cc == 7 ? (uint8_t)(16 | KA) : 0;
-                    else if (r == 2) v = 16 | FU;
-                    else if (r == 6) v = FU;
-                    else if (r == 7) v = cc == 1 ? KA : cc == 7 ? HI : 0;
-                    else if (r == 8) v = bk;
+            if (kLoad) {
+                for (int s = lane; s < 96; s += 32) S.abs_[s] = s < 81 ? p.load_board[b * 96 + s] : (uint8_t)0;
+                if (lane < 16) hand[lane] = lane < 14 ? p.load_misc[b * 16 + lane] : (uint8_t)0;
+                stm = p.load_misc[b * 16 + 14] & 1;
+            } else {
+                constexpr uint64_t back = 0x234585432ull;   // KY KE GI KI OU KI GI KE KY, nibble c = file c
+                for (int s = lane; s < 96; s += 32) {
+                    uint8_t v = 0;
+                    if (s < 81) {
+                        int r = s / 9, cc = s - 9 * r;
+                        const uint8_t bk = (uint8_t)((back >> (4 * cc)) & 15u);
+                        if (r == 0) v = (uint8_t)(16 | bk);
+                        else if (r == 1) v = cc == 1 ? (uint8_t)(16 | HI) : cc == 7 ? (uint8_t)(16 | KA) : 0;
+                        else if (r == 2) v = 16 | FU;
+                        else if (r == 6) v = FU;
+                        else if (r == 7) v = cc == 1 ? KA : cc == 7 ? HI : 0;
+                        else if (r == 8) v = bk;
+                    }
+                    S.abs_[s] = v;
                 }
-                S.abs_[s] = v;
+                if (lane < 16) hand[lane] = 0;
+                stm = 0;
             }
-            if (lane < 16) hand[lane] = 0;
-            stm = 0; step = 0;
+            step = 0;
             __syncwarp();
         } else {
             const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)cur, 1);
@@ -732,8 +745,12 @@ __global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st
 }
 
 static int launch(const Params& p, cudaStream_t s) {
-    const int64_t grid = persistent_grid(step_kernel, kWarps * 32, 0, (p.n + kWarps - 1) / kWarps);
-    step_kernel<<<(unsigned)grid, kWarps * 32, 0, s>>>(p);
+    const int64_t need = (p.n + kWarps - 1) / kWarps;
+    if (p.load_board) {
+        step_kernel<true><<<(unsigned)persistent_grid(step_kernel<true>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+    } else {
+        step_kernel<false><<<(unsigned)persistent_grid(step_kernel<false>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+    }
     return (int)cudaGetLastError();
 }
 
@@ -747,6 +764,17 @@ int bbk_shogi_init(const bbk_cols* out, const bbk_shogi_state* out_s, int64_t n,
     shogi::Params p{};
     p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
     p.max_steps = max_steps; p.force_reset = 1;
+    return shogi::launch(p, (cudaStream_t)stream);
+}
+
+int bbk_shogi_load(const bbk_cols* out, const bbk_shogi_state* out_s, const uint8_t* boards, const uint8_t* misc,
+                   int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys, int32_t max_steps,
+                   void* stream) {
+    if (n <= 0) return 0;
+    if (!boards || !misc) return (int)cudaErrorInvalidValue;
+    shogi::Params p{};
+    p.out = *out; p.out_s = *out_s; p.slot_keys = slot_keys; p.n = n; p.slot0 = slot0; p.key = key_state;
+    p.max_steps = max_steps; p.force_reset = 1; p.load_board = boards; p.load_misc = misc;
     return shogi::launch(p, (cudaStream_t)stream);
 }
 

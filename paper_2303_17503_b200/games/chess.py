@@ -18,9 +18,43 @@ import numpy as np
 
 from .. import _native as nat
 from ..core import GameDef, GameSpec, StaleBatch
+from ..rng import key_state
 from ._device import DeviceKernel, DeviceV, Lineage, _torch
 
 HIST_BYTES = 128 * 32 + 128 * 4
+
+_FEN_TYPES = {"p": 1, "n": 2, "b": 3, "r": 4, "q": 5, "k": 6}
+
+
+def parse_fen(fen: str) -> tuple[bytes, bytes]:
+    """FEN -> (board[64] piece codes colour << 3 | P1 N2 B3 R4 Q5 K6, a1 = 0; misc[8] = side to move,
+    castling bits (1 K, 2 Q, 4 k, 8 q), en-passant square (int8, -1 none), half-move clock).
+
+    The layout bbk_chess_load takes (DESIGN.md §3.3 conventions; same reading as the oracle's
+    test hook orc_chess_set_fen). Raises ValueError on a malformed placement field."""
+    parts = fen.split()
+    board = bytearray(64)
+    r, f = 7, 0
+    for ch in parts[0]:
+        if ch == "/":
+            r, f = r - 1, 0
+        elif ch.isdigit():
+            f += int(ch)
+        else:
+            t = _FEN_TYPES.get(ch.lower())
+            if t is None or not (0 <= r < 8 and 0 <= f < 8):
+                raise ValueError(f"bad FEN placement: {parts[0]!r}")
+            board[r * 8 + f] = (8 if ch.islower() else 0) | t
+            f += 1
+    stm = 1 if len(parts) > 1 and parts[1] == "b" else 0
+    castle = 0
+    for ch in parts[2] if len(parts) > 2 else "":
+        castle |= {"K": 1, "Q": 2, "k": 4, "q": 8}.get(ch, 0)
+    ep = -1
+    if len(parts) > 3 and parts[3] != "-":
+        ep = (int(parts[3][1]) - 1) * 8 + (ord(parts[3][0]) - ord("a"))
+    half = int(parts[4]) if len(parts) > 4 else 0
+    return bytes(board), bytes([stm, castle, ep & 0xFF, min(half, 255), 0, 0, 0, 0])
 
 
 class RingStore:
@@ -78,12 +112,48 @@ class RingKernel(DeviceKernel):
         return S(nat.ptr(v.priv.board[i:i + 1]), nat.ptr(v.priv.misc[i:i + 1]), nat.ptr(v.store.hist[i:i + 1]))
 
     def launch_init(self, v, ks, sk):
-        torch = _torch()
-        v.store = RingStore(torch.empty((v.n, self.hist_bytes), dtype=torch.uint8, device=v.device))
+        v.store = self.alloc_store(v)
         v.store.lineage = Lineage(v.uid)
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_init")
         nat.check(fn(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                      nat.stream_handle(v.device)), f"bbk_{self.prefix}_init")
+
+    def parse_position(self, text: str) -> tuple[bytes, bytes]:
+        raise NotImplementedError
+
+    def alloc_store(self, v):
+        torch = _torch()
+        return RingStore(torch.empty((v.n, self.hist_bytes), dtype=torch.uint8, device=v.device))
+
+    def load(self, gdef, positions, key=None, limit: int | None = None, slot0: int = 0, device=None,
+             obs: bool = True) -> DeviceV:
+        """A batch whose slot i starts from positions[i] (FEN / SFEN text or a (board, misc) byte pair):
+        step_count 0, empty history, player_to_role from the slot key as in init (bbk_<game>_load).
+
+        There is no reference counterpart (the reference has no chess / shogi engine); this is the
+        device twin of the oracle's set_fen / set_sfen test hooks and what the device perft and
+        rule-position tests drive."""
+        torch = _torch()
+        pairs = [self.parse_position(p) if isinstance(p, str) else p for p in positions]
+        if not pairs:
+            from ..core import EmptyBatch
+
+            raise EmptyBatch("no positions")
+        limit = gdef.max_steps if limit is None else int(limit)
+        device = self._device(device)
+        n = len(pairs)
+        boards = torch.tensor(np.frombuffer(b"".join(b for b, _ in pairs), dtype=np.uint8).reshape(n, -1)).to(device)
+        misc = torch.tensor(np.frombuffer(b"".join(m for _, m in pairs), dtype=np.uint8).reshape(n, -1)).to(device)
+        if boards.shape[1] != self.board_bytes or misc.shape[1] != self.misc_bytes:
+            raise ValueError(f"{self.game_id}: positions must be {self.board_bytes} + {self.misc_bytes} bytes")
+        v = self.new_v(n, slot0, device, 0, limit, obs)
+        v.store = self.alloc_store(v)
+        v.store.lineage = Lineage(v.uid)
+        fn = getattr(nat.lib(), f"bbk_{self.prefix}_load")
+        nat.check(fn(self.cols(v), self.state_struct(v), nat.ptr(boards), nat.ptr(misc), n, slot0,
+                     0 if key is None else key_state(key), None, limit, nat.stream_handle(device)),
+                  f"bbk_{self.prefix}_load")
+        return v
 
     def prepare_step(self, v, out):
         lin = v.store.lineage
@@ -131,6 +201,9 @@ class ChessKernel(RingKernel):
     obs_shape = (8, 8, 119)
     hist_bytes = HIST_BYTES
     board_bytes = 64
+
+    def parse_position(self, text):
+        return parse_fen(text)
 
     def core_view(self, s, i, p2r, rewards, mask, terminal):
         m = s["misc"][i]

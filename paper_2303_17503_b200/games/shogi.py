@@ -16,7 +16,51 @@ from __future__ import annotations
 from .. import _native as nat
 from ..core import GameDef, GameSpec
 from ._device import DeviceV, Lineage, _torch
-from .chess import RingKernel, RingStore
+from .chess import RingKernel, RingStore  # noqa: F401
+
+
+_SFEN_TYPES = {"p": 1, "l": 2, "n": 3, "s": 4, "g": 5, "b": 6, "r": 7, "k": 8}
+_PROMOTE = {1: 9, 2: 10, 3: 11, 4: 12, 6: 13, 7: 14}
+_HAND = "plnsgbr"
+
+
+def parse_sfen(sfen: str) -> tuple[bytes, bytes]:
+    """SFEN -> (board[96] absolute codes owner << 4 | FU1 KY2 KE3 GI4 KI5 KA6 HI7 OU8 TO9 NY10 NK11
+    NG12 UM13 RY14, square r*9+c with r = 0 the top rank and c = 0 file 9; misc[16] = hands [2][7]
+    (FU KY KE GI KI KA HI), side to move (1 = White / gote), 0).
+
+    The layout bbk_shogi_load takes (same reading as orc_shogi_set_sfen)."""
+    parts = sfen.split()
+    board = bytearray(96)
+    r = c = 0
+    prom = False
+    for ch in parts[0]:
+        if ch == "/":
+            r, c = r + 1, 0
+        elif ch.isdigit():
+            c += int(ch)
+        elif ch == "+":
+            prom = True
+        else:
+            t = _SFEN_TYPES.get(ch.lower())
+            if t is None or r > 8 or c > 8 or (prom and t not in _PROMOTE):
+                raise ValueError(f"bad SFEN placement: {parts[0]!r}")
+            board[r * 9 + c] = (16 if ch.islower() else 0) | (_PROMOTE[t] if prom else t)
+            c, prom = c + 1, False
+    misc = bytearray(16)
+    misc[14] = 1 if len(parts) > 1 and parts[1] == "w" else 0
+    cnt = 0
+    for ch in parts[2] if len(parts) > 2 else "-":
+        if ch == "-":
+            break
+        if ch.isdigit():
+            cnt = cnt * 10 + int(ch)
+            continue
+        if ch.lower() not in _HAND:
+            raise ValueError(f"bad SFEN hand: {parts[2]!r}")
+        misc[(7 if ch.islower() else 0) + _HAND.index(ch.lower())] += cnt or 1
+        cnt = 0
+    return bytes(board), bytes(misc)
 
 
 class ShogiCoreView:
@@ -52,10 +96,16 @@ class ShogiKernel(RingKernel):
         return nat.ShogiState(nat.ptr(v.priv.board[i:i + 1]), nat.ptr(v.priv.misc[i:i + 1]), nat.ptr(h[i:i + 1]),
                               h.shape[1])
 
-    def launch_init(self, v, ks, sk):
+    def parse_position(self, text):
+        return parse_sfen(text)
+
+    def alloc_store(self, v):
         torch = _torch()
         # per env: position keys by ply (max_steps + 2) then a 2048-bit repetition Bloom filter (32 x u64)
-        v.store = RingStore(torch.empty((v.n, int(v.limit) + 2 + 32), dtype=torch.int64, device=v.device))
+        return RingStore(torch.empty((v.n, int(v.limit) + 2 + 32), dtype=torch.int64, device=v.device))
+
+    def launch_init(self, v, ks, sk):
+        v.store = self.alloc_store(v)
         v.store.lineage = Lineage(v.uid)
         nat.check(nat.lib().bbk_shogi_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                            nat.stream_handle(v.device)), "bbk_shogi_init")
