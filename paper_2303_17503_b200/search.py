@@ -51,6 +51,9 @@ def _unit(t) -> int:
 
 def copy_rows(src_tensors, dst_tensors, src_idx, dst_idx, n: int, stream) -> None:
     """dst[dst_idx[i]] = src[src_idx[i]] for every per-slot tensor pair (bbk_copy_rows)."""
+    for idx in (src_idx, dst_idx):
+        if idx is not None and (idx.dtype != _torch().int32 or not idx.is_contiguous()):
+            raise ValueError("bbk_copy_rows takes contiguous int32 row indices")
     pairs = list(zip(src_tensors, dst_tensors))
     for k in range(0, len(pairs), nat.ROW_COPY_MAX):
         chunk = pairs[k:k + nat.ROW_COPY_MAX]

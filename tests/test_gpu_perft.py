@@ -46,8 +46,9 @@ CHESS_KATS = [
     (POS5, [44, 1486, 62379]),
     (POS6, [46, 2079, 89890]),
 ]
-# one level deeper for the positions whose next level stays under ~100 k device rows
+# one level deeper (the deepest level stepped on the device holds 9,467-197,281 rows)
 CHESS_DEEP = [
+    (CHESS_START, 4865609),   # level 4 = 197,281 device rows
     (KIWIPETE, 4085603),
     (POS3, 674624),
     (POS4, 422333),
@@ -132,7 +133,7 @@ def expand(kern, gdef, v):
     w = kern.new_v(n2, 0, v.device, v.t, v.limit, obs=True)
     w.store = v.store.like(n2)
     w.store.lineage = Lineage(w.uid)
-    src = torch.from_numpy(parents.astype(np.int64)).to(v.device)
+    src = torch.from_numpy(parents.astype(np.int32)).to(v.device)
     copy_rows(kern.row_tensors(v), kern.row_tensors(w), src, None, n2, nat.stream_handle(v.device))
     out = kern.step(gdef, w, actions.astype(np.int64), bb.RngKey(1), v.limit)
     return out, parents, actions
@@ -162,7 +163,7 @@ def test_chess_device_perft(oracle, fen, counts):
     run_perft(oracle, "chess", fen, counts)
 
 
-@pytest.mark.parametrize("fen,count", CHESS_DEEP, ids=["kiwipete", "pos3", "pos4", "pos5", "pos6"])
+@pytest.mark.parametrize("fen,count", CHESS_DEEP, ids=["start", "kiwipete", "pos3", "pos4", "pos5", "pos6"])
 def test_chess_device_perft_one_deeper(oracle, fen, count):
     run_perft(oracle, "chess", fen, dict(CHESS_KATS)[fen], extra=count)
 
