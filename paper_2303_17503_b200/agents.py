@@ -32,8 +32,18 @@ def random_actions_device(batch, key: RngKey, out=None):
 
 
 def random_actions(batch, key: RngKey) -> np.ndarray:
-    """Host-array version with the reference's return type (agents.py:33-46)."""
-    return random_actions_device(batch, key).cpu().numpy()
+    """Host-array version with the reference's return type (agents.py:33-46).
+
+    Always a fresh array: when the fused sampler wrote into a caller's pinned host buffer, the
+    launching stream is synchronised first (the kernel writes it asynchronously) and the buffer
+    is copied, so the result neither races the kernel nor aliases a buffer the caller reuses."""
+    a = random_actions_device(batch, key)
+    if a.device.type == "cpu":
+        import torch
+
+        torch.cuda.current_stream(batch._v.device).synchronize()
+        return a.numpy().copy()
+    return a.cpu().numpy()
 
 
 class RolloutResult:

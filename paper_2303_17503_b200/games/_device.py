@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import sys
+import threading
 import weakref
 from types import SimpleNamespace
 
@@ -34,11 +35,16 @@ def _torch():
 
 
 _UID = [0]
+_UID_LOCK = threading.Lock()
+_POOLS_LOCK = threading.Lock()
+# per-thread fused outputs of the launch being built (the kernel objects are shared per game)
+_TLS = threading.local()
 
 
 def _next_uid() -> int:
-    _UID[0] += 1
-    return _UID[0]
+    with _UID_LOCK:
+        _UID[0] += 1
+        return _UID[0]
 
 
 class Lineage:
@@ -46,15 +52,24 @@ class Lineage:
 
     Games with an in-place per-env history (Go superko store, chess/shogi
     repetition rings) share it along a trajectory. ``head`` is the newest
-    batch; ``trail`` its predecessors (newest first). Stepping the head is
-    the fast path; stepping a recent predecessor is a branch (the game
-    decides whether that needs a private copy); anything older raises
-    StaleBatch.
+    batch, ``trail`` its predecessors (newest first), ``head_t`` the head's
+    step index. Stepping the head is the fast path; stepping a predecessor is a
+    branch: the game copies the store first, so the original trajectory stays
+    steppable (reference states are pure values, core.py:1-7).
+
+    ``append_only``: no step of this lineage could have auto-reset a slot (only
+    scalar ``core.step`` calls, which refuse finished states, advanced it). Every
+    predecessor's history prefix is then still intact, so any of them can be
+    branched (the trail is kept in full). Once a batch step runs, resets may have
+    rewritten a slot's history, and only the last ``keep`` predecessors stay
+    branchable (the games' depth limits); anything older raises StaleBatch.
     """
 
-    def __init__(self, uid: int):
+    def __init__(self, uid: int, t: int = 0, append_only: bool = True):
         self.head = uid
+        self.head_t = t
         self.trail: list[int] = []
+        self.append_only = append_only
 
     def depth(self, uid: int) -> int:
         if uid == self.head:
@@ -64,13 +79,21 @@ class Lineage:
         except ValueError:
             return 1 << 30
 
-    def advance(self, parent: int, child: int, keep: int = 2) -> None:
+    def mark_batch_step(self, keep: int = 2) -> None:
+        if self.append_only:
+            self.append_only = False
+            self.trail = self.trail[:keep]
+
+    def advance(self, parent: int, child: int, keep: int = 2, child_t: int | None = None) -> None:
+        lim = None if self.append_only else keep
         if parent == self.head:
-            self.trail = ([parent] + self.trail)[:keep]
-        else:   # branch: the old head (and anything newer than parent) is dropped
+            self.trail = ([parent] + self.trail)[:lim]
+        else:   # branch in place: the old head (and anything newer than parent) is dropped
             i = self.trail.index(parent)
-            self.trail = self.trail[i:i + keep]
+            self.trail = self.trail[i:] if lim is None else self.trail[i:i + lim]
         self.head = child
+        if child_t is not None:
+            self.head_t = child_t
 
 
 class DeviceV:
@@ -136,8 +159,6 @@ def _recycle(pool: list, vd: dict) -> None:
     the reuse safe exactly as for torch's caching allocator. This removes the ~16 allocations and
     the pointer-struct rebuild from every public step call (the e2e path's host overhead).
     """
-    if len(pool) >= POOL_DEPTH:
-        return
     dev, priv = vd.get("dev"), vd.get("priv")
     if dev is None or priv is None:
         return
@@ -147,7 +168,9 @@ def _recycle(pool: list, vd: dict) -> None:
             # references: the namespace, the loop variable, getrefcount's argument
             if t is not None and (sys.getrefcount(t) != 3 or use_count(t.untyped_storage()._cdata) != 2):
                 return
-    pool.append((dev, priv, {k: vd[k] for k in _CACHED if k in vd}))
+    with _POOLS_LOCK:
+        if len(pool) < POOL_DEPTH:
+            pool.append((dev, priv, {k: vd[k] for k in _CACHED if k in vd}))
 
 
 class DeviceKernel:
@@ -164,12 +187,13 @@ class DeviceKernel:
         stream when one is pooled (see _recycle), else freshly allocated."""
         torch = _torch()
         v = DeviceV(self, n, slot0, device, t, limit)
-        pools = self.__dict__.setdefault("_pools", {})
         stream = torch.cuda.current_stream(device).cuda_stream if torch.device(device).type == "cuda" else 0
         pkey = (n, device, obs, stream)
-        pool = pools.setdefault(pkey, [])
-        if pool:
-            v.dev, v.priv, cached = pool.pop()
+        with _POOLS_LOCK:
+            pool = self.__dict__.setdefault("_pools", {}).setdefault(pkey, [])
+            got = pool.pop() if pool else None
+        if got is not None:
+            v.dev, v.priv, cached = got
             v.__dict__.update(cached)
         else:
             self._alloc_columns(v, obs)
@@ -239,11 +263,11 @@ class DeviceKernel:
         v = self.new_v(n, slot0, device, 0, limit, obs)
         sk = self._slot_keys(slot_keys, device)
         ks = 0 if key is None else key_state(key)
-        self._fused = self._fused_args(v, next_key, next_actions, episodes)
+        _TLS.fused = self._fused_args(v, next_key, next_actions, episodes)
         try:
             self.launch_init(v, ks, sk)
         finally:
-            self._fused = None
+            _TLS.fused = None
         return v
 
     def _fused_args(self, v, next_key, next_actions, episodes):
@@ -266,7 +290,7 @@ class DeviceKernel:
                 episodes)
 
     def out_cols(self, v: DeviceV) -> nat.Cols:
-        return self.cols(v, getattr(self, "_fused", None))
+        return self.cols(v, getattr(_TLS, "fused", None))
 
     # -------------------------------------------------------- protocol: step
     def as_actions(self, actions, v: DeviceV):
@@ -306,10 +330,15 @@ class DeviceKernel:
             raise IllegalAction(f"slot {slot}: illegal action {act} in {self.game_id}", action=act, slot=slot)
 
     def step(self, gdef, v: DeviceV, actions, key, limit: int, validate: bool = True, slot_keys=None,
-             out: DeviceV | None = None, next_key=None, next_actions=None, episodes=None) -> DeviceV:
+             out: DeviceV | None = None, next_key=None, next_actions=None, episodes=None,
+             scalar: bool = False) -> DeviceV:
+        """``scalar``: the caller guarantees no slot of v is finished (core.step), so no slot
+        resets and the trajectory's history store stays append-only (see Lineage)."""
         a = self.as_actions(actions, v)
         if validate:
             self.validate(v, a)
+        if v.store is not None and not scalar:
+            v.store.lineage.mark_batch_step(self.branch_keep)
         sk = self._slot_keys(slot_keys, v.device)
         ks = 0 if key is None else key_state(key)
         if out is None:
@@ -322,16 +351,39 @@ class DeviceKernel:
             out.next_actions = None
             out.next_key = None
         self.prepare_step(v, out)
-        self._fused = self._fused_args(out, next_key, next_actions, episodes)
+        _TLS.fused = self._fused_args(out, next_key, next_actions, episodes)
         try:
             self.launch_step(v, out, a, ks, sk, limit)
         finally:
-            self._fused = None
+            _TLS.fused = None
         return out
 
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
         """Hook for games with shared in-place stores (Go, chess, shogi)."""
         out.store = v.store
+
+    # ------------------------------------------------ branching (shared per-env stores)
+    branch_keep = 2   # predecessors a batch-stepped lineage keeps branchable
+
+    def branch_depth(self, v: DeviceV) -> int:
+        """How far v is behind the head of its store's lineage (0 = head); raises StaleBatch when
+        the shared store may no longer hold v's history."""
+        from ..core import StaleBatch
+
+        if v.store is None or v.store.lineage is None:
+            return 0
+        lin = v.store.lineage
+        d = lin.depth(v.uid)
+        if d == 0:
+            return 0
+        if d >= (1 << 30) or (d > self.branch_keep and not lin.append_only):
+            raise StaleBatch(f"{self.game_id}: batch is too far behind its trajectory (only the newest batch and "
+                             f"its last {self.branch_keep} predecessors remain steppable after a batch step)")
+        self.check_branch(v, lin)
+        return d
+
+    def check_branch(self, v: DeviceV, lin: Lineage) -> None:
+        """Game hook: extra validity conditions of a branch (chess: ring wrap)."""
 
     # ----------------------------------------------------- protocol: state_at
     def host_snapshot(self, v: DeviceV) -> dict:
@@ -455,7 +507,7 @@ class DeviceKernel:
         v and out share v's per-env store (updated in place)."""
         out.store = v.store
         out._host = {}
-        self._fused = None
+        _TLS.fused = None
         self.launch_step(v, out, a, 0, slot_keys, limit)
 
     # subclasses

@@ -155,14 +155,17 @@ class RingKernel(DeviceKernel):
                   f"bbk_{self.prefix}_load")
         return v
 
+    branch_keep = 1   # after a batch step only the newest batch's predecessor is branchable
+
     def prepare_step(self, v, out):
-        lin = v.store.lineage
-        depth = lin.depth(v.uid)
-        if depth > 1:
-            raise StaleBatch(f"{self.game_id}: only the newest batch and its predecessor can be stepped "
-                             "(the repetition ring is shared in place)")
-        out.store = v.store
-        lin.advance(v.uid, out.uid)
+        depth = self.branch_depth(v)
+        store = v.store
+        if depth > 0:   # branch: private copy, the original trajectory stays steppable
+            old = store.lineage
+            store = RingStore(store.hist.clone())
+            store.lineage = Lineage(v.uid, v.t, old.append_only)
+        out.store = store
+        store.lineage.advance(v.uid, out.uid, self.branch_keep, out.t)
 
     def launch_step(self, v, out, a, ks, sk, limit):
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_step")
@@ -189,8 +192,9 @@ class RingKernel(DeviceKernel):
         return {"board": v.priv.board.cpu().numpy(), "misc": v.priv.misc.cpu().numpy()}
 
     def slice_store(self, v, w, i):
+        self.branch_depth(v)   # StaleBatch if stepping v's descendants overwrote its history
         w.store = RingStore(v.store.hist[i:i + 1].clone())
-        w.store.lineage = Lineage(w.uid)
+        w.store.lineage = Lineage(w.uid, w.t)
 
 
 class ChessKernel(RingKernel):
@@ -204,6 +208,18 @@ class ChessKernel(RingKernel):
 
     def parse_position(self, text):
         return parse_fen(text)
+
+    def check_branch(self, v, lin):
+        """The 128-ply ring is reused modulo 128: stepping v reads plies [t + 1 - M, t] (M = the
+        half-move window, at least the 7 observation plies), which later plies of the lineage
+        overwrite once the head is 128 plies past the window's start."""
+        from ..core import StaleBatch
+
+        hm = int(v.priv.misc[:, 3].max().item())
+        M = max(hm + 1, 7)
+        if lin.head_t - (v.t + 1 - M) >= 128:
+            raise StaleBatch("chess: the repetition ring no longer holds this batch's history (more than 128 "
+                             "plies behind)")
 
     def core_view(self, s, i, p2r, rewards, mask, terminal):
         m = s["misc"][i]

@@ -32,7 +32,7 @@ class GoCoreView:
     """Host view of one slot with the reference Core's fields (go.py:83-111)."""
 
     __slots__ = ("board", "role_to_move", "terminal", "rewards", "mask", "pass_count", "hash", "hist_xor",
-                 "hist_len", "boards_hist")
+                 "hist_len", "boards_hist", "_src", "_history")
 
     def __init__(self, board, role_to_move, terminal, rewards, mask, pass_count, hash_, hist_xor, hist_len,
                  boards_hist):
@@ -46,6 +46,20 @@ class GoCoreView:
         self.hist_xor = hist_xor
         self.hist_len = hist_len
         self.boards_hist = boards_hist
+        self._src = None
+        self._history = None
+
+    @property
+    def history(self) -> frozenset:
+        """The superko set (reference ``Core.history``, go.py:83-100): the slot's prefix of the
+        device history store, read on first access. Raises StaleBatch when the batch is too far
+        behind its lineage for the shared store to still hold its prefix."""
+        if self._history is None:
+            if self._src is None:
+                raise AttributeError("history: core view is not attached to a device batch")
+            v, i = self._src
+            self._history = v.kern.history_of(v, i, self.hist_len)
+        return self._history
 
     def encode(self) -> bytes:
         """Byte-identical to reference Core.encode (go.py:103-111)."""
@@ -82,6 +96,13 @@ class GoStore:
         if st is None:
             st = self._struct = nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
         return st
+
+
+def _with_store(v: DeviceV, store) -> DeviceV:
+    """A shallow stand-in of v whose store is `store` (v's private state, the copy's filters)."""
+    from types import SimpleNamespace
+
+    return SimpleNamespace(store=store, priv=v.priv, n=v.n, device=v.device)
 
 
 class GoKernel(DeviceKernel):
@@ -132,23 +153,28 @@ class GoKernel(DeviceKernel):
         nat.check(nat.lib().bbk_go_init(self.size, cols, st, store, v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_go_init")
 
+    branch_keep = 2   # a live slot's history prefix survives two batch steps (see history_of)
+
+    def rebuild_filters(self, w: DeviceV) -> None:
+        """Recompute the Bloom / count-pair filters of w's store from its history prefixes
+        (bbk_go_rebuild_bloom): after a branch copied a store that later steps may have added to."""
+        nat.check(nat.lib().bbk_go_rebuild_bloom(w.store.struct(), nat.ptr(w.priv.hist_len), w.n,
+                                                 nat.stream_handle(w.device)), "bbk_go_rebuild_bloom")
+
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
         store = v.store
         if out.limit + 2 > store.hist_cap:
             raise ValueError("max_steps exceeds the history capacity of this batch")
-        depth = store.lineage.depth(v.uid)
-        if depth > 2:
-            raise StaleBatch("batch is too far behind its lineage; only the last two predecessors of the "
-                             "newest batch can be stepped again")
+        depth = self.branch_depth(v)
         if depth > 0:
             # branch: private copy of the history, filters rebuilt for v's lengths; the
-            # original lineage keeps its store
+            # original lineage keeps its store (and stays steppable)
+            old = store.lineage
             store = GoStore(store.history.clone(), store.bloom.clone(), store.hist_cap)
-            store.lineage = Lineage(v.uid)
-            nat.check(nat.lib().bbk_go_rebuild_bloom(store.struct(), nat.ptr(v.priv.hist_len), v.n,
-                                                     nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
+            store.lineage = Lineage(v.uid, v.t, old.append_only)
+            self.rebuild_filters(_with_store(v, store))
         out.store = store
-        store.lineage.advance(v.uid, out.uid)
+        store.lineage.advance(v.uid, out.uid, self.branch_keep, out.t)
 
     def launch_step(self, v, out, a, ks, sk, limit) -> None:
         nat.check(nat.lib().bbk_go_step(self.size, self.komi, int(self.allow_self_capture), self.cols(v), self.state_struct(v), self.out_cols(out),
@@ -172,15 +198,25 @@ class GoKernel(DeviceKernel):
         return super().observe_at(gdef, v, i, role)
 
     def slice_store(self, v: DeviceV, w: DeviceV, i: int) -> None:
+        depth = self.branch_depth(v)
         s = v.store
         w.store = GoStore(s.history[i:i + 1].clone(), s.bloom[i:i + 1].clone(), s.hist_cap)
-        w.store.lineage = Lineage(w.uid)
-        depth = s.lineage.depth(v.uid)
+        w.store.lineage = Lineage(w.uid, w.t)
         if depth > 0:
-            if depth > 2:
-                raise StaleBatch("batch too far behind its lineage to slice")
-            nat.check(nat.lib().bbk_go_rebuild_bloom(w.store.struct(), nat.ptr(w.priv.hist_len), 1,
-                                                     nat.stream_handle(v.device)), "bbk_go_rebuild_bloom")
+            self.rebuild_filters(w)
+
+    def history_of(self, v: DeviceV, i: int, hist_len: int) -> frozenset:
+        """Slot i's superko set: entries [0, hist_len) of the shared append-only store. A live slot's
+        prefix survives while the batch is at most two steps behind the lineage head (a reset
+        rewrites entry 0 with the same value 0, the next placement entry 1)."""
+        self.branch_depth(v)   # raises StaleBatch when the store may no longer hold v's prefix
+        row = v.store.history[i, :hist_len].cpu().numpy().view(np.uint64)
+        return frozenset(int(x) for x in row)
+
+    def state_at(self, gdef, v, i, limit):
+        st = super().state_at(gdef, v, i, limit)
+        st.core._src = (v, i)
+        return st
 
     def core_view(self, s, i, p2r, rewards, mask, terminal):
         pat = s["pat"][i].view(np.uint16)[: self.cells].astype(np.uint32)

@@ -1,0 +1,149 @@
+"""Value semantics of device states (reference core.py:1-7: states are immutable values and step is
+a pure function) under the shared per-trajectory history stores (Go superko, chess ring, shogi key
+log), plus the host-side thread-safety of the shared kernel objects.
+
+* scalar trajectories (core.init / core.step) never auto-reset, so their stores are append-only:
+  ANY earlier state can be stepped again (the reference's mcts_agent re-steps stored node states),
+  and the original trajectory stays steppable afterwards;
+* batch trajectories keep the newest batch and its last predecessors steppable (Go two, chess /
+  shogi one) and raise StaleBatch beyond, never a silently wrong state;
+* search() and slicing honour the same rule.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2303_17503_b200 as bb
+from paper_2303_17503_b200.agents import random_actions
+from paper_2303_17503_b200.core import StaleBatch
+
+pytestmark = pytest.mark.gpu
+
+GAMES = ("go_9x9", "go_19x19", "chess", "shogi", "backgammon")
+
+
+def _walk(game, key, n_steps):
+    st = [bb.init(game, key.child(0))]
+    acts = []
+    for t in range(1, n_steps + 1):
+        s = st[-1]
+        if s.terminated or s.truncated:
+            break
+        legal = np.flatnonzero(s.legal_action_mask)
+        a = int(legal[key.child(2 * t).randint(len(legal))])
+        acts.append(a)
+        st.append(bb.step(s, a, key.child(2 * t + 1)))
+    return st, acts
+
+
+@pytest.mark.parametrize("game", GAMES)
+def test_scalar_states_branch_at_any_depth(game):
+    key = bb.RngKey(41)
+    states, acts = _walk(game, key, 40)
+    assert len(states) > 12
+    for j in (1, 4, len(states) // 2):   # re-step an old state with a different legal action
+        s = states[j]
+        legal = np.flatnonzero(s.legal_action_mask)
+        a = int(legal[-1])
+        got = bb.step(s, a, key.child(2 * (j + 1) + 1))
+        # reference semantics: identical to replaying the same actions from a fresh init
+        r = bb.init(game, key.child(0))
+        for t, b in enumerate(acts[:j], start=1):
+            r = bb.step(r, b, key.child(2 * t + 1))
+        want = bb.step(r, a, key.child(2 * (j + 1) + 1))
+        assert bb.state_fingerprint(got) == bb.state_fingerprint(want), (game, j)
+        assert np.array_equal(bb.observe(got, 0), bb.observe(want, 0))
+    # ... and the original trajectory is untouched: its head steps on like before
+    head = states[-1]
+    if not (head.terminated or head.truncated):
+        a = int(np.flatnonzero(head.legal_action_mask)[0])
+        bb.step(head, a, key.child(999))
+        states2, _ = _walk(game, key, len(states) - 1)
+        for x, y in zip(states, states2):
+            assert bb.state_fingerprint(x) == bb.state_fingerprint(y)
+
+
+@pytest.mark.parametrize("game,keep", [("go_9x9", 2), ("go_19x19", 2), ("chess", 1), ("shogi", 1)])
+def test_batch_lineage_branch_limits(game, keep):
+    root = bb.RngKey(3)
+    b = [bb.batch_init(game, root.child(0), 64)]
+    for t in range(1, 6):
+        b.append(bb.batch_step(b[-1], random_actions(b[-1], root.child(2 * t - 1)), root.child(2 * t)))
+    # depth <= keep: branching works and equals a from-scratch replay; the old head stays steppable
+    d = keep
+    src = b[-1 - d]
+    acts = random_actions(src, root.child(777))
+    got = bb.batch_step(src, acts, root.child(778))
+    r = bb.batch_init(game, root.child(0), 64)
+    for t in range(1, 6 - d):
+        r = bb.batch_step(r, random_actions(r, root.child(2 * t - 1)), root.child(2 * t))
+    want = bb.batch_step(r, acts, root.child(778))
+    assert bb.batch_fingerprint(got) == bb.batch_fingerprint(want)
+    assert np.array_equal(got.observation, want.observation)
+    nxt = bb.batch_step(b[-1], random_actions(b[-1], root.child(11)), root.child(12))
+    assert nxt.size == 64
+    # deeper than keep: StaleBatch (never a silently wrong state)
+    with pytest.raises(StaleBatch):
+        bb.batch_step(b[-2 - keep], random_actions(b[-2 - keep], root.child(5)), root.child(6))
+
+
+def test_search_on_a_predecessor_batch_equals_search_before_stepping():
+    from paper_2303_17503_b200.agents import mcts_actions
+
+    root = bb.RngKey(9)
+    b = bb.batch_init("go_9x9", root.child(0), 16)
+    for t in range(1, 30):
+        b = bb.batch_step(b, random_actions(b, root.child(2 * t - 1)), root.child(2 * t))
+    live = ~(b.terminated | b.truncated)
+    assert live.all()
+    before = np.asarray(mcts_actions(b, root.child(100), 8))
+    b1 = bb.batch_step(b, random_actions(b, root.child(101)), root.child(102))
+    b2 = bb.batch_step(b1, random_actions(b1, root.child(103)), root.child(104))
+    after = np.asarray(mcts_actions(b, root.child(100), 8))   # b is two steps behind now
+    assert np.array_equal(before, after)
+    bb.batch_step(b2, random_actions(b2, root.child(105)), root.child(106))
+    with pytest.raises(StaleBatch):
+        mcts_actions(b, root.child(100), 8)
+
+
+def test_threads_stepping_the_same_game_match_a_sequential_run():
+    """One kernel object per game is shared by every caller: launches from several threads (each
+    with its own fused next-actions buffer) must not see each other's pointers."""
+    import torch
+
+    def run(seed, out, idx):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            sess = bb.BatchSession("go_9x9", 512, seed)
+            prints = []
+            for _ in range(40):
+                sess.step(sess.sample_random_actions())
+                prints.append(bb.batch_fingerprint(sess.batch))
+        out[idx] = prints
+
+    seq = [None] * 4
+    for i in range(4):
+        run(i, seq, i)
+    par = [None] * 4
+    th = [threading.Thread(target=run, args=(i, par, i)) for i in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert par == seq
+
+
+def test_random_actions_into_pinned_buffer_is_synchronised_and_copied():
+    import torch
+
+    root = bb.RngKey(4)
+    b = bb.batch_init("chess", root.child(0), 4096)
+    buf = torch.empty(4096, dtype=torch.int64).pin_memory()
+    nxt = bb.batch_step(b, random_actions(b, root.child(1)), root.child(2), next_key=root.child(3), next_actions=buf)
+    got = random_actions(nxt, root.child(3))
+    want = np.asarray(nxt._v.kern.random_actions(nxt._v, root.child(3)).cpu())
+    assert np.array_equal(got, want)
+    assert not np.shares_memory(got, buf.numpy())
