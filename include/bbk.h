@@ -189,7 +189,8 @@ int bbk_random_actions(const uint8_t* mask, int64_t n, int32_t num_actions, uint
 
 /* IllegalAction check (core.py:234-239, tictactoe.py:111-121): writes the
  * lowest live slot whose action is out of range or masked out into
- * *first_bad (initialise it to INT32_MAX), finished slots are exempt. */
+ * *first_bad, or INT32_MAX when every live action is legal (a plain store:
+ * no initialisation needed); finished slots are exempt. One launch. */
 int bbk_check_actions(const uint8_t* mask, const uint8_t* terminated, const uint8_t* truncated,
                       const int64_t* actions, int64_t n, int32_t num_actions, int32_t* first_bad,
                       void* stream);

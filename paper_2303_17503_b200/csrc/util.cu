@@ -3,6 +3,7 @@
 //   bbk_check_actions   -- IllegalAction detection (core.py:234-239, tictactoe.py:111-121)
 //   bbk_count_finished  -- episode counter of bench_run (bench.py:129)
 //   bbk_latch_finished  -- first-episode returns / lengths of a batched rollout (agents.py:113-116)
+#include <climits>
 #include "common.cuh"
 #include "../../include/bbk.h"
 
@@ -71,14 +72,26 @@ __global__ void random_actions_kernel(const uint8_t* mask, int64_t n, int A, uin
     }
 }
 
-__global__ void check_actions_kernel(const uint8_t* mask, const uint8_t* term, const uint8_t* trunc,
-                                     const int64_t* actions, int64_t n, int A, int32_t* first_bad) {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= n) return;
-    if (term[b] || trunc[b]) return;
-    int64_t a = actions[b];
-    bool bad = a < 0 || a >= A || !mask[b * (int64_t)A + a];
-    if (bad) atomicMin(first_bad, (int32_t)b);
+// One CTA: the lowest live offending slot (or INT32_MAX) by a grid-stride scan and a block min,
+// written with a plain store -- the caller needs no initialisation launch (a single kernel per check).
+__global__ void __launch_bounds__(1024) check_actions_kernel(const uint8_t* mask, const uint8_t* term,
+                                                             const uint8_t* trunc, const int64_t* actions, int64_t n,
+                                                             int A, int32_t* first_bad) {
+    __shared__ int32_t wmin[32];
+    int32_t best = INT32_MAX;
+    for (int64_t b = threadIdx.x; b < n && b < best; b += blockDim.x) {
+        if (term[b] || trunc[b]) continue;
+        const int64_t a = actions[b];
+        if (a < 0 || a >= A || !mask[b * (int64_t)A + a]) best = (int32_t)b;   // b increases per thread
+    }
+    best = __reduce_min_sync(BBK_FULL, best);
+    if (lane_id() == 0) wmin[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int32_t v = threadIdx.x < (blockDim.x >> 5) ? wmin[threadIdx.x] : INT32_MAX;
+        v = __reduce_min_sync(BBK_FULL, v);
+        if (threadIdx.x == 0) *first_bad = v;
+    }
 }
 
 __global__ void count_finished_kernel(const uint8_t* term, const uint8_t* trunc, int64_t n,
@@ -131,7 +144,7 @@ int bbk_random_actions(const uint8_t* mask, int64_t n, int32_t num_actions, uint
 int bbk_check_actions(const uint8_t* mask, const uint8_t* terminated, const uint8_t* truncated,
                       const int64_t* actions, int64_t n, int32_t num_actions, int32_t* first_bad, void* stream) {
     if (n <= 0) return 0;
-    util::check_actions_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+    util::check_actions_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
         mask, terminated, truncated, actions, n, num_actions, first_bad);
     return (int)cudaGetLastError();
 }

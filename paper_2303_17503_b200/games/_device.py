@@ -319,7 +319,11 @@ class DeviceKernel:
     def validate(self, v: DeviceV, a) -> None:
         """IllegalAction with the lowest offending live slot (tictactoe.py:111-121)."""
         torch = _torch()
-        bad = torch.full((1,), INT32_MAX, dtype=torch.int32, device=v.device)
+        bkey = (v.device, nat.stream_handle(v.device))
+        with _POOLS_LOCK:   # one result word per (device, stream); bbk_check_actions stores it (no fill launch)
+            bad = self.__dict__.setdefault("_bad", {}).get(bkey)
+            if bad is None:
+                bad = self._bad[bkey] = torch.empty(1, dtype=torch.int32, device=v.device)
         d = v.dev
         nat.check(nat.lib().bbk_check_actions(nat.ptr(d.legal_action_mask), nat.ptr(d.terminated),
                                               nat.ptr(d.truncated), nat.ptr(a), v.n, self.num_actions,
