@@ -8,8 +8,10 @@ HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def names():
-    """Trajectory fixtures (make_golden*.py); the search fixtures are listed by search_names()."""
-    return sorted(f[:-5] for f in os.listdir(HERE) if f.endswith(".json") and not f.startswith("mcts_"))
+    """Trajectory fixtures (make_golden*.py); the search fixtures are listed by search_names(),
+    the CLI trace fixture (make_golden_cli.py) is read by test_gpu_cli.py."""
+    return sorted(f[:-5] for f in os.listdir(HERE)
+                  if f.endswith(".json") and not f.startswith(("mcts_", "cli_")))
 
 
 def search_names():
