@@ -201,6 +201,7 @@ def bench_run(config: BenchConfig) -> BenchResult:
 
 _BENCH_FIELDS = ("game_id", "batch_size", "total_steps", "seed", "threads", "wall_seconds", "samples_per_second",
                  "episodes_completed")
+_MATCH_FIELDS = ("game_id", "agent_a", "agent_b", "wins_a", "wins_b", "draws")
 
 
 def _fmt(v):
@@ -208,16 +209,20 @@ def _fmt(v):
 
 
 def write_results(results, path, kind: str | None = None) -> None:
-    """CSV of BenchResults with the reference's fixed header (bench.py:118-135)."""
+    """CSV of BenchResults or agents.MatchResults with the reference's fixed headers
+    (bench.py:158-179; the kind defaults from the first row's type)."""
     rows = list(results)
-    if kind not in (None, "bench"):
-        raise ValueError("only bench results are produced here (match results need the out-of-scope agents)")
+    if kind is None:
+        kind = "matches" if rows and hasattr(rows[0], "wins_a") else "bench"
+    if kind not in ("bench", "matches"):
+        raise ValueError(f"unknown result kind {kind!r}")
+    fields = _MATCH_FIELDS if kind == "matches" else _BENCH_FIELDS
     try:
         with open(path, "w", newline="") as fh:
             w = csv.writer(fh)
-            w.writerow(_BENCH_FIELDS)
+            w.writerow(fields)
             for row in rows:
-                w.writerow([_fmt(getattr(row, f)) for f in _BENCH_FIELDS])
+                w.writerow([_fmt(getattr(row, f)) for f in fields])
     except OSError as exc:
         raise IoError(f"cannot write {path}: {exc}") from exc
 

@@ -121,6 +121,12 @@ def test_bench_config_results_and_csv(tmp_path):
     assert len((tmp_path / "l.csv").read_text().splitlines()) == 5
     with pytest.raises(bb.IoError):
         bb.write_results([r], tmp_path / "missing" / "x.csv")
+    # match results (bench.py:162-170): the kind follows the row type
+    from paper_2303_17503_b200.agents import MatchResult
+
+    m = tmp_path / "m.csv"
+    bb.write_results([MatchResult("tic_tac_toe", "random", "mcts", 3, 5, 2)], m)
+    assert m.read_text().splitlines() == ["game_id,agent_a,agent_b,wins_a,wins_b,draws", "tic_tac_toe,random,mcts,3,5,2"]
 
 
 def _toy_kernel():
