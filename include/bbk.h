@@ -34,7 +34,8 @@
 extern "C" {
 #endif
 
-#define BBK_ABI_VERSION 4   /* 3: bbk_go_state.lab, fingerprints, small engines; 4: batched UCT search */
+#define BBK_ABI_VERSION 5   /* 3: bbk_go_state.lab, fingerprints, small engines; 4: batched UCT search;
+                               5: per-size Go superko filters (bbk_go_filter_words, size arg of bbk_go_rebuild_bloom) */
 
 typedef struct bbk_cols {
     float*    observation;        /* may be NULL: skip observation emission */
@@ -64,9 +65,11 @@ typedef struct bbk_cols {
  *   lab[n, pat_stride]  uint16: chain label per stone = one point of the stone's chain
  *                       (maintained incrementally; values at empty points are don't-care)
  *   history[n, hist_cap] uint64 append-only superko hashes (history set)
- *   bloom[n, 320]        uint32: 8192-bit Bloom filter over history hashes, then a
- *                        2048-bit filter of the (black, white) stone-count pairs of the
- *                        history positions (a repeat must have equal counts)
+ *   bloom[n, bbk_go_filter_words(size)] uint32: a Bloom filter over history hashes, then a
+ *                        filter of the (black, white) stone-count pairs of the history
+ *                        positions (a repeat must have equal counts). Sized per board:
+ *                        2048 + 1024 bits up to 9x9, 4096 + 1024 up to 13x13, else the
+ *                        8192 + 2048 bits below (the largest).
  */
 #define BBK_GO_BLOOM_WORDS 256
 #define BBK_GO_PAIR_WORDS 64
@@ -89,6 +92,8 @@ typedef struct bbk_go_store {
 } bbk_go_store;
 
 int bbk_go_pat_stride(int size);
+/* uint32 words of one env's superko filter row (-1 for an unsupported size) */
+int bbk_go_filter_words(int size);
 
 /* batch_init (core.py:340-350) */
 int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
@@ -107,7 +112,7 @@ int bbk_go_step(int size, double komi, int allow_self_capture, const bbk_cols* i
 int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, void* stream);
 
 /* Rebuild Bloom filters from history[0:hist_len) (used when a batch branches). */
-int bbk_go_rebuild_bloom(const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream);
+int bbk_go_rebuild_bloom(int size, const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream);
 
 /* ---------------------------------------------------------- Backgammon --
  * Replaces games/backgammon.py: _legal_mask :62-95, _roll :125-130,

@@ -97,7 +97,8 @@ def _declare(L):
     sig("bbk_go_step", [C.c_int, C.c_double, C.c_int, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),
                         P, I64, I64, U64, P, I32, P])
     sig("bbk_go_observe", [C.c_int, P, P, P, I64, P])
-    sig("bbk_go_rebuild_bloom", [ptr(GoStore), P, I64, P])
+    sig("bbk_go_filter_words", [C.c_int])
+    sig("bbk_go_rebuild_bloom", [C.c_int, ptr(GoStore), P, I64, P])
     sig("bbk_bg_init", [ptr(Cols), ptr(BgState), I64, I64, U64, P, I32, P])
     sig("bbk_bg_step", [ptr(Cols), ptr(BgState), ptr(Cols), ptr(BgState), P, I64, I64, U64, P, I32, P])
     sig("bbk_bg_observe", [ptr(BgState), P, P, I64, P])

@@ -35,7 +35,15 @@ using namespace bbk;
 
 constexpr int kWarps = 4;             // warps (boards in flight) per CTA
 constexpr int kPlanes = 17;
-constexpr int kBloomBits = BBK_GO_BLOOM_WORDS * 32;   // 8192
+
+// Superko filter of one env, sized per board: it is read whole every step, so its size is HBM
+// traffic (1,280 B at 19x19 against a 25.9 KB step, but 21 % of a 9x9 step at that size). The
+// history of a small board is short (random 9x9 games end after ~130 plies), so a 2048-bit Bloom
+// filter keeps the false-positive rate (answered by the exact history scan) well under 1 %.
+__host__ __device__ constexpr int bloom_words(int N) { return N <= 9 ? 64 : N <= 13 ? 128 : BBK_GO_BLOOM_WORDS; }
+__host__ __device__ constexpr int pair_words(int N) { return N <= 13 ? 32 : BBK_GO_PAIR_WORDS; }
+__host__ __device__ constexpr int filter_words(int N) { return bloom_words(N) + pair_words(N); }
+__host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
 
 __host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
 
@@ -58,13 +66,13 @@ struct WarpSmem {
         struct {
             // the board's chain labels (u16) until the run list is built; then the env's
             // Bloom + count-pair filter (cp.async)
-            alignas(16) uint32_t bl[BBK_GO_FILTER_WORDS];
+            alignas(16) uint32_t bl[filter_words(N)];
             uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
             uint16_t root[MAXR];   // chain label of the run
             uint32_t gst[C];       // OR(lib) | OR(~lib) << 10 | HAS, by chain label
         } uf;
         struct {
-            uint32_t bloom_area[BBK_GO_FILTER_WORDS];
+            uint32_t bloom_area[filter_words(N)];
             uint64_t hit[32];
         } sk;
         alignas(16) uint8_t mb[((A + 47) & ~15)];
@@ -73,7 +81,7 @@ struct WarpSmem {
             uint32_t W[(C * 17 + 31) / 32 + 2];
         } ob;
     } u;
-    static_assert(2 * pat_stride(N) <= 4 * BBK_GO_FILTER_WORDS, "labels must fit the filter landing area");
+    static_assert(2 * pat_stride(N) <= 4 * filter_words(N), "labels must fit the filter landing area");
     static_assert(pf_off(N) + 4 * pat_stride(N) <= (int)sizeof(u), "pat + lab prefetch must fit the union");
     alignas(16) uint16_t pat[pat_stride(N)];
     uint32_t rX[32], rY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
@@ -121,27 +129,32 @@ __device__ __forceinline__ uint32_t run_at(uint32_t X, int s) {
     return ((1u << len) - 1u) << s;
 }
 
+template <int N>
 __device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
-    uint32_t i1 = (uint32_t)h & (kBloomBits - 1);
-    uint32_t i2 = (uint32_t)(h >> 13) & (kBloomBits - 1);
-    uint32_t i3 = (uint32_t)(h >> 26) & (kBloomBits - 1);
+    constexpr uint32_t M = 32u * bloom_words(N) - 1u;
+    uint32_t i1 = (uint32_t)h & M;
+    uint32_t i2 = (uint32_t)(h >> 13) & M;
+    uint32_t i3 = (uint32_t)(h >> 26) & M;
     return ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & (bloom[i3 >> 5] >> (i3 & 31)) & 1u) != 0;
 }
 
 // Stone-count pair filter: a position can only repeat a history position with the same
 // (black, white) stone counts; all non-capture candidates of a board share one pair.
+template <int N>
 __device__ __forceinline__ uint32_t pair_idx(int nb, int nw) {
-    return ((uint32_t)((nb << 9) | nw) * 0x9E3779B1u) >> 21;   // 11 bits
+    return ((uint32_t)((nb << 9) | nw) * 0x9E3779B1u) >> (32 - log2i(32 * pair_words(N)));
 }
+template <int N>
 __device__ __forceinline__ void pair_add(uint32_t* gb, int nb, int nw) {   // lane 0 only
-    const uint32_t i = pair_idx(nb, nw);
-    atomicOr(&gb[BBK_GO_BLOOM_WORDS + (i >> 5)], 1u << (i & 31));
+    const uint32_t i = pair_idx<N>(nb, nw);
+    atomicOr(&gb[bloom_words(N) + (i >> 5)], 1u << (i & 31));
 }
 
 // Lane 0 only: add h to the env's global filter.
+template <int N>
 __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
-    const uint32_t idx[3] = {(uint32_t)h & (kBloomBits - 1), (uint32_t)(h >> 13) & (kBloomBits - 1),
-                             (uint32_t)(h >> 26) & (kBloomBits - 1)};
+    constexpr uint32_t M = 32u * bloom_words(N) - 1u;
+    const uint32_t idx[3] = {(uint32_t)h & M, (uint32_t)(h >> 13) & M, (uint32_t)(h >> 26) & M};
 #pragma unroll
     for (int j = 0; j < 3; j++) atomicOr(&gb[idx[j] >> 5], 1u << (idx[j] & 31));   // RED: no round trip
 }
@@ -255,7 +268,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         __threadfence_block();
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.bl);
         const char* src = reinterpret_cast<const char*>(gbloom);
-        for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
+        for (int i = lane; i < filter_words(N) / 4; i += 32)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
         asm volatile("cp.async.commit_group;");
     }
@@ -329,8 +342,8 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     bool pair_seen;
     {
         const int mb = ycol == 1 ? nblack + 1 : nblack, mw = ycol == 1 ? nwhite : nwhite + 1;   // mover = 1 - ycol
-        const uint32_t i = pair_idx(mb, mw);
-        pair_seen = (bl[BBK_GO_BLOOM_WORDS + (i >> 5)] >> (i & 31)) & 1u;
+        const uint32_t i = pair_idx<N>(mb, mw);
+        pair_seen = (bl[bloom_words(N) + (i >> 5)] >> (i & 31)) & 1u;
     }
     if (!pair_seen) {
         legal = cand & ~capb;
@@ -342,7 +355,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         int cell = r * N + p;
         uint64_t h2 = ((sc >> p) & 1u) ? h : h ^ zkey<N>(cell, 1 - ycol);
         if (((capb | sc) >> p) & 1u) h2 ^= S.capx[cell];
-        if (bloom_maybe(bl, h2)) pend |= 1u << p;
+        if (bloom_maybe<N>(bl, h2)) pend |= 1u << p;
         else legal |= 1u << p;
     }
     while (__any_sync(BBK_FULL, pend != 0u)) {
@@ -504,10 +517,10 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     bool pat_ready = false;
 
     for (int64_t b = b0; b < p.n; b += nwarps) {
-        if (!p.force_reset && b + nwarps < p.n && lane < 10) {
+        if (!p.force_reset && b + nwarps < p.n && lane < (4 * filter_words(N) + 127) / 128) {
             // warm L2 with the next board's Bloom filter (cp.async'd mid-board)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)BBK_GO_FILTER_WORDS) + 128 * lane));
+                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)filter_words(N)) + 128 * lane));
         }
         const uint64_t f_term = __shfl_sync(BBK_FULL, (uint32_t)pf, 0), f_trunc = __shfl_sync(BBK_FULL, (uint32_t)pf, 1);
         const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)pf, 2), f_role = __shfl_sync(BBK_FULL, (uint32_t)pf, 3);
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         const bool reset = p.force_reset || f_term || f_trunc;
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
-        uint32_t* gbloom = p.store.bloom + b * (int64_t)BBK_GO_FILTER_WORDS;
+        uint32_t* gbloom = p.store.bloom + b * (int64_t)filter_words(N);
         int8_t p2r0, p2r1;
         int role, pass_count, step, hlen;
         uint64_t h, hx;
@@ -536,10 +549,10 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             // the discarded prefetch of this board must land before the scratch is reused
             if (pat_ready) asm volatile("cp.async.wait_all;" ::: "memory");
             for (int i = lane; i < PS; i += 32) { S.pat[i] = 0; lab[i] = 0; }
-            for (int i = lane; i < BBK_GO_FILTER_WORDS / 4; i += 32)
+            for (int i = lane; i < filter_words(N) / 4; i += 32)
                 reinterpret_cast<uint4*>(gbloom)[i] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
-            if (lane == 0) { bloom_add(gbloom, 0ull); pair_add(gbloom, 0, 0); hist[0] = 0ull; }
+            if (lane == 0) { bloom_add<N>(gbloom, 0ull); pair_add<N>(gbloom, 0, 0); hist[0] = 0ull; }
             nscan = 0; extra = 0ull;
         } else {
             p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
@@ -675,8 +688,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 const int nbk = counts & 0xFFFF, nwh = counts >> 16;
                 if (lane == 0) {
                     hist[hlen] = h2;
-                    bloom_add(gbloom, h2);
-                    pair_add(gbloom, nbk, nwh);
+                    bloom_add<N>(gbloom, h2);
+                    pair_add<N>(gbloom, nbk, nwh);
                 }
                 nscan = hlen; extra = h2;
                 hlen += 1; h = h2; hx ^= h2; pass_count = 0;
@@ -821,27 +834,28 @@ __global__ void __launch_bounds__(kWarps * 32) observe_kernel(const uint16_t* pa
     }
 }
 
+template <int N>
 __global__ void rebuild_bloom_kernel(bbk_go_store st, const int32_t* hist_len, int64_t n) {
-    __shared__ uint32_t sb[kWarps][BBK_GO_BLOOM_WORDS];
+    constexpr int BW = bloom_words(N), FW = filter_words(N);
+    constexpr uint32_t M = 32u * BW - 1u;
+    __shared__ uint32_t sb[kWarps][BW];
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * kWarps;
     for (int64_t b = (int64_t)blockIdx.x * kWarps + w; b < n; b += nwarps) {
-        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) sb[w][i] = 0u;
+        for (int i = lane; i < BW; i += 32) sb[w][i] = 0u;
         __syncwarp();
         const uint64_t* hist = st.history + b * (int64_t)st.hist_cap;
         for (int j = lane; j < hist_len[b]; j += 32) {
             uint64_t h = hist[j];
-            uint32_t i1 = (uint32_t)h & (kBloomBits - 1), i2 = (uint32_t)(h >> 13) & (kBloomBits - 1),
-                     i3 = (uint32_t)(h >> 26) & (kBloomBits - 1);
+            uint32_t i1 = (uint32_t)h & M, i2 = (uint32_t)(h >> 13) & M, i3 = (uint32_t)(h >> 26) & M;
             atomicOr(&sb[w][i1 >> 5], 1u << (i1 & 31));
             atomicOr(&sb[w][i2 >> 5], 1u << (i2 & 31));
             atomicOr(&sb[w][i3 >> 5], 1u << (i3 & 31));
         }
         __syncwarp();
-        for (int i = lane; i < BBK_GO_BLOOM_WORDS; i += 32) st.bloom[b * BBK_GO_FILTER_WORDS + i] = sb[w][i];
+        for (int i = lane; i < BW; i += 32) st.bloom[b * FW + i] = sb[w][i];
         // history keeps no stone counts: mark every pair as seen (correct, only slower)
-        for (int i = lane; i < BBK_GO_PAIR_WORDS; i += 32)
-            st.bloom[b * BBK_GO_FILTER_WORDS + BBK_GO_BLOOM_WORDS + i] = 0xFFFFFFFFu;
+        for (int i = BW + lane; i < FW; i += 32) st.bloom[b * FW + i] = 0xFFFFFFFFu;
         __syncwarp();
     }
 }
@@ -922,6 +936,11 @@ extern "C" {
 
 int bbk_go_pat_stride(int size) { return go::pat_stride(size); }
 
+int bbk_go_filter_words(int size) {
+    if (size < 5 || size > 19 || !(size & 1)) return -1;
+    return go::filter_words(size);
+}
+
 int bbk_go_init(int size, const bbk_cols* out, const bbk_go_state* out_s, const bbk_go_store* store,
                 int64_t n, int64_t slot0, uint64_t key_state, const uint64_t* slot_keys,
                 int32_t max_steps, void* stream) {
@@ -960,11 +979,23 @@ int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* ob
     }
 }
 
-int bbk_go_rebuild_bloom(const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream) {
+int bbk_go_rebuild_bloom(int size, const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream) {
     if (n <= 0) return 0;
     int64_t grid = (n + go::kWarps - 1) / go::kWarps;
     if (grid > 148 * 8) grid = 148 * 8;
-    go::rebuild_bloom_kernel<<<(unsigned)grid, go::kWarps * 32, 0, (cudaStream_t)stream>>>(*store, hist_len, n);
+    const dim3 g((unsigned)grid), t(go::kWarps * 32);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (size) {
+        case 5: go::rebuild_bloom_kernel<5><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 7: go::rebuild_bloom_kernel<7><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 9: go::rebuild_bloom_kernel<9><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 11: go::rebuild_bloom_kernel<11><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 13: go::rebuild_bloom_kernel<13><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 15: go::rebuild_bloom_kernel<15><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 17: go::rebuild_bloom_kernel<17><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        case 19: go::rebuild_bloom_kernel<19><<<g, t, 0, s>>>(*store, hist_len, n); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
     return (int)cudaGetLastError();
 }
 

@@ -117,6 +117,8 @@ class GoKernel(DeviceKernel):
         self.obs_shape = (size, size, 2 * HISTORY_PLANES + 1)
         self.game_id = f"go_{size}x{size}"
         self.pat_stride = (self.cells + 7) & ~7
+        # superko filter row (u32 words): Bloom + stone-count pairs, sized per board (go.cu filter_words)
+        self.filter_words = (64 if size <= 9 else 128 if size <= 13 else 256) + (32 if size <= 13 else 64)
 
     def alloc_private(self, v: DeviceV) -> None:
         torch = _torch()
@@ -143,7 +145,7 @@ class GoKernel(DeviceKernel):
         torch = _torch()
         cap = int(limit) + 2
         hist = torch.empty((n, cap), dtype=torch.int64, device=device)
-        bloom = torch.empty((n, 320), dtype=torch.int32, device=device)   # BBK_GO_FILTER_WORDS
+        bloom = torch.empty((n, self.filter_words), dtype=torch.int32, device=device)
         return GoStore(hist, bloom, cap)
 
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
@@ -158,7 +160,7 @@ class GoKernel(DeviceKernel):
     def rebuild_filters(self, w: DeviceV) -> None:
         """Recompute the Bloom / count-pair filters of w's store from its history prefixes
         (bbk_go_rebuild_bloom): after a branch copied a store that later steps may have added to."""
-        nat.check(nat.lib().bbk_go_rebuild_bloom(w.store.struct(), nat.ptr(w.priv.hist_len), w.n,
+        nat.check(nat.lib().bbk_go_rebuild_bloom(self.size, w.store.struct(), nat.ptr(w.priv.hist_len), w.n,
                                                  nat.stream_handle(w.device)), "bbk_go_rebuild_bloom")
 
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:

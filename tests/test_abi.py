@@ -26,7 +26,12 @@ def test_library_exports_every_declared_symbol():
     L = _native.lib()
     missing = [s for s in declared_symbols() if not hasattr(L, s)]
     assert not missing, missing
-    assert L.bbk_abi_version() == 4
+    assert L.bbk_abi_version() == 5
+    from paper_2303_17503_b200.games.go import GoKernel
+
+    for n in (5, 7, 9, 11, 13, 15, 17, 19):   # host allocation == kernel row stride
+        assert L.bbk_go_filter_words(n) == GoKernel(n).filter_words
+    assert L.bbk_go_filter_words(8) == -1
 
 
 def test_library_is_sm100a():
