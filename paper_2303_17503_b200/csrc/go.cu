@@ -1,13 +1,14 @@
 // Go (Tromp-Taylor, positional superko) batched step for sm_100a.
 //
 // Replaces reference pkg/src/boardbatch/games/go.py for make_game(size)
-// (size 9 and 19 instantiated): apply :219-262, _analyse :45-80,
+// (odd sizes 5..19 instantiated): apply :219-262, _analyse :45-80,
 // legal_mask :121-174, score_rewards :176-210, init_core :212-217,
 // observe :264-273, plus env-core _make_state core.py:192-220 and the
 // auto-reset of batch_step core.py:353-386.
 //
-// Mapping: one warp per board, lane r owns board row r as bit rows
-// (black, white, empty; bit c = column c). Per step:
+// Mapping: one warp SEGMENT per board -- a whole warp for 15x15..19x19, half a
+// warp (16 lanes, two boards per warp) up to 13x13 -- and segment lane r owns
+// board row r as bit rows (black, white, empty; bit c = column c). Per step:
 //   1. placement + captures: bit-parallel flood of each enemy neighbour
 //      group over the rows (shuffles), captured iff no liberty;
 //   2. analysis of the new board: chains carry a persistent label (one point
@@ -18,8 +19,8 @@
 //   3. legal mask: empty points with an empty neighbour / a non-atari own
 //      neighbour group / a capture (XOR of the captured atari groups'
 //      zobrist accumulated at their single liberty), filtered by positional
-//      superko through a per-env 8192-bit Bloom filter with an exact scan of
-//      the append-only history on a Bloom hit (identical answers to the
+//      superko through a per-env Bloom filter with an exact scan of the
+//      append-only history on a Bloom hit (identical answers to the
 //      reference's `h2 not in history`);
 //   4. observation: the 8-deep board history is kept TRANSPOSED per point
 //      (uint16 `pat`, bit 2t/2t+1 = black/white in boards_hist[t]), so the
@@ -33,8 +34,14 @@
 namespace go {
 using namespace bbk;
 
-constexpr int kWarps = 4;             // warps (boards in flight) per CTA
+constexpr int kWarps = 4;             // warps per CTA
 constexpr int kPlanes = 17;
+
+// Lanes per board. Rows are lanes, so a 9x9 board on a whole warp keeps 9 of 32 lanes busy in
+// every row-parallel phase; on half a warp (two independent boards per warp, each with its own
+// 16-lane shuffle / ballot / syncwarp mask, so the halves may diverge) it keeps 9 of 16.
+__host__ __device__ constexpr int seg_lanes(int N) { return N <= 13 ? 16 : 32; }
+__host__ __device__ constexpr int boards_per_cta(int N) { return kWarps * (32 / seg_lanes(N)); }
 
 // Superko filter of one env, sized per board: it is read whole every step, so its size is HBM
 // traffic (1,280 B at 19x19 against a 25.9 KB step, but 21 % of a 9x9 step at that size). The
@@ -54,10 +61,71 @@ __host__ __device__ constexpr int pf_off(int N) {
     return ((ob > mb ? ob : mb) + 15) & ~15;
 }
 
+// The lanes of one board: shuffles / votes / syncs over the segment's mask only (width L), so the
+// two boards of a split warp never wait on each other.
+template <int L>
+struct Seg {
+    unsigned m;   // the segment's lanes
+    int sl;       // lane within the segment (the row it owns)
+    __device__ __forceinline__ Seg() {
+        const int lane = lane_id();
+        sl = lane & (L - 1);
+        if constexpr (L == 32) m = BBK_FULL;
+        else m = ((1u << L) - 1u) << (lane & ~(L - 1));
+    }
+    __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) const { return __shfl_sync(m, v, src, L); }
+    __device__ __forceinline__ int shfl(int v, int src) const { return __shfl_sync(m, v, src, L); }
+    __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) const {
+        const uint32_t lo = __shfl_sync(m, (uint32_t)v, src, L), hi = __shfl_sync(m, (uint32_t)(v >> 32), src, L);
+        return ((uint64_t)hi << 32) | lo;
+    }
+    __device__ __forceinline__ bool any(bool p) const { return __any_sync(m, p); }
+    // segment-relative ballot (bit i = segment lane i)
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        const unsigned v = __ballot_sync(m, p);
+        if constexpr (L == 32) return v;
+        else return (v & m) >> (__ffs(m) - 1);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(m); }
+    __device__ __forceinline__ unsigned reduce_or(unsigned v) const { return __reduce_or_sync(m, v); }
+    __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+        for (int o = L / 2; o; o >>= 1) v += __shfl_xor_sync(m, v, o, L);
+        return v;
+    }
+    __device__ __forceinline__ uint64_t xor64(uint64_t v) const {
+#pragma unroll
+        for (int o = L / 2; o; o >>= 1) {
+            const uint32_t lo = __shfl_xor_sync(m, (uint32_t)v, o, L);
+            const uint32_t hi = __shfl_xor_sync(m, (uint32_t)(v >> 32), o, L);
+            v ^= ((uint64_t)hi << 32) | lo;
+        }
+        return v;
+    }
+    // inclusive prefix sum over the segment lanes
+    __device__ __forceinline__ int scan(int v) const {
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) {
+            const int t = __shfl_up_sync(m, v, o, L);
+            if (sl >= o) v += t;
+        }
+        return v;
+    }
+    __device__ __forceinline__ uint32_t up_row(uint32_t v) const {   // row r-1's value at row r
+        const uint32_t u = __shfl_up_sync(m, v, 1, L);
+        return sl > 0 ? u : 0u;
+    }
+    __device__ __forceinline__ uint32_t dn_row(uint32_t v) const {   // row r+1's value at row r
+        const uint32_t d = __shfl_down_sync(m, v, 1, L);
+        return sl < L - 1 ? d : 0u;
+    }
+};
+
 template <int N>
-struct WarpSmem {
+struct WarpSmem {   // one board's scratch (one per segment)
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
+    static constexpr int L = seg_lanes(N);
     static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
     uint64_t capx[C];
     // Phase-multiplexed scratch (each member is dead before the next one is written):
@@ -73,7 +141,7 @@ struct WarpSmem {
         } uf;
         struct {
             uint32_t bloom_area[filter_words(N)];
-            uint64_t hit[32];
+            uint64_t hit[L];
         } sk;
         alignas(16) uint8_t mb[((A + 47) & ~15)];
         struct {
@@ -83,9 +151,10 @@ struct WarpSmem {
     } u;
     static_assert(2 * pat_stride(N) <= 4 * filter_words(N), "labels must fit the filter landing area");
     static_assert(pf_off(N) + 4 * pat_stride(N) <= (int)sizeof(u), "pat + lab prefetch must fit the union");
+    static_assert(N <= L, "a board's rows must fit its lanes");
     alignas(16) uint16_t pat[pat_stride(N)];
-    uint32_t rX[32], rY[32], rE[32], rcap[32];   // rX/rY double as rowB/rowW
-    int32_t roff[33];
+    uint32_t rX[L], rY[L], rE[L], rcap[L];   // rX/rY double as rowB/rowW and the flat stone bitmaps
+    static_assert(L == 32 || 4 * L >= pat_stride(N) / 8 + 8, "flat stone bitmaps must fit rX / rY");
 };
 
 // zobrist key of (cell, colour) (go.py:20-25): mix64(0x60D00D60C0FFEE00 + N + 2*cell + colour).
@@ -106,7 +175,7 @@ template <int N>
 struct BlockSmem {
     static constexpr int C = N * N;
     float4 lut[16];
-    WarpSmem<N> w[kWarps];
+    WarpSmem<N> w[boards_per_cta(N)];
 };
 
 struct StepParams {
@@ -145,12 +214,12 @@ __device__ __forceinline__ uint32_t pair_idx(int nb, int nw) {
     return ((uint32_t)((nb << 9) | nw) * 0x9E3779B1u) >> (32 - log2i(32 * pair_words(N)));
 }
 template <int N>
-__device__ __forceinline__ void pair_add(uint32_t* gb, int nb, int nw) {   // lane 0 only
+__device__ __forceinline__ void pair_add(uint32_t* gb, int nb, int nw) {   // one lane only
     const uint32_t i = pair_idx<N>(nb, nw);
     atomicOr(&gb[bloom_words(N) + (i >> 5)], 1u << (i & 31));
 }
 
-// Lane 0 only: add h to the env's global filter.
+// One lane only: add h to the env's global filter.
 template <int N>
 __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
     constexpr uint32_t M = 32u * bloom_words(N) - 1u;
@@ -159,38 +228,30 @@ __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
     for (int j = 0; j < 3; j++) atomicOr(&gb[idx[j] >> 5], 1u << (idx[j] & 31));   // RED: no round trip
 }
 
-__device__ __forceinline__ uint32_t up_row(uint32_t v, int lane) {
-    uint32_t u = __shfl_up_sync(BBK_FULL, v, 1);
-    return lane > 0 ? u : 0u;
-}
-__device__ __forceinline__ uint32_t dn_row(uint32_t v, int lane) {
-    uint32_t d = __shfl_down_sync(BBK_FULL, v, 1);
-    return lane < 31 ? d : 0u;
-}
-template <int N>
-__device__ __forceinline__ uint32_t dilate(uint32_t F, int lane) {
+template <int N, int L>
+__device__ __forceinline__ uint32_t dilate(const Seg<L>& g, uint32_t F) {
     constexpr uint32_t ROW = (1u << N) - 1u;
-    return ((F << 1) | (F >> 1) | up_row(F, lane) | dn_row(F, lane)) & ROW;
+    return ((F << 1) | (F >> 1) | g.up_row(F) | g.dn_row(F)) & ROW;
 }
 
 // Tromp-Taylor area score (go.py:176-210), bit-parallel: an empty region
 // borders colour X iff it is reachable through empties from a point adjacent
 // to X. Returns role rewards (black, white).
-template <int N>
-__device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0, float& r1) {
+template <int N, int L>
+__device__ void score(const Seg<L>& g, uint32_t Bk, uint32_t Wh, double komi, float& r0, float& r1) {
     constexpr uint32_t ROW = (1u << N) - 1u;
-    const uint32_t rowm = lane < N ? ROW : 0u;
+    const uint32_t rowm = g.sl < N ? ROW : 0u;
     uint32_t E = ~(Bk | Wh) & rowm;
-    uint32_t RB = dilate<N>(Bk, lane) & E, RW = dilate<N>(Wh, lane) & E;
+    uint32_t RB = dilate<N>(g, Bk) & E, RW = dilate<N>(g, Wh) & E;
     while (true) {
-        uint32_t nb = (RB | dilate<N>(RB, lane)) & E;
-        uint32_t nw = (RW | dilate<N>(RW, lane)) & E;
-        bool ch = __any_sync(BBK_FULL, (nb != RB) || (nw != RW));
+        uint32_t nb = (RB | dilate<N>(g, RB)) & E;
+        uint32_t nw = (RW | dilate<N>(g, RW)) & E;
+        bool ch = g.any((nb != RB) || (nw != RW));
         RB = nb; RW = nw;
         if (!ch) break;
     }
-    int black = warp_sum(__popc(Bk) + __popc(E & RB & ~RW));
-    int white = warp_sum(__popc(Wh) + __popc(E & RW & ~RB));
+    int black = g.sum(__popc(Bk) + __popc(E & RB & ~RW));
+    int white = g.sum(__popc(Wh) + __popc(E & RW & ~RB));
     double b = black, w = white + komi;
     if (b > w) { r0 = 1.0f; r1 = -1.0f; }
     else if (w > b) { r0 = -1.0f; r1 = 1.0f; }
@@ -202,30 +263,23 @@ __device__ void score(uint32_t Bk, uint32_t Wh, double komi, int lane, float& r0
 // E = empties (row bits of this lane).
 //
 // Group analysis (go.py:45-80 restated for what the mask needs): every
-// horizontal run of stones is a union-find node. Runs are laid out as a flat
-// list (row-major, X runs then Y runs per row) so that the union / flatten /
-// liberty / classification passes stride lanes over RUNS, not rows -- the work
-// is balanced no matter how the stones are distributed over the rows.
-template <int N>
-__device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y, uint32_t E, uint64_t h,
-                               const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra,
-                               int nblack, int nwhite, bool self_capture, int lane) {
+// horizontal run of stones is a node. Runs are laid out as a flat list
+// (row-major, X runs then Y runs per row) so that the liberty / classification
+// passes stride lanes over RUNS, not rows -- the work is balanced no matter how
+// the stones are distributed over the rows.
+template <int N, int L>
+__device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y, uint32_t E,
+                               uint64_t h, const uint64_t* hist, const uint32_t* gbloom, int nscan, uint64_t extra,
+                               int nblack, int nwhite, bool self_capture) {
     constexpr uint32_t ROW = (1u << N) - 1u;
     auto& U = S.u.uf;
-    const int r = lane;
+    const int r = g.sl;
     const uint32_t SX = X & ~(X << 1), SY = Y & ~(Y << 1);
     const int nx = __popc(SX), cnt = nx + __popc(SY);
-    int off = cnt;   // exclusive prefix sum of run counts over rows
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(BBK_FULL, off, o);
-        if (lane >= o) off += t;
-    }
-    const int total = __shfl_sync(BBK_FULL, off, 31);
+    int off = g.scan(cnt);   // inclusive prefix sum of run counts over rows
+    const int total = g.shfl(off, L - 1);
     off -= cnt;
-    S.rX[lane] = X; S.rY[lane] = Y; S.rE[lane] = E; S.rcap[lane] = 0u;
-    S.roff[lane] = off;
-    if (lane == 31) S.roff[32] = total;
+    S.rX[r] = X; S.rY[r] = Y; S.rE[r] = E; S.rcap[r] = 0u;
     {   // this row's runs -> list, each with its chain label
         const uint16_t* lab = reinterpret_cast<const uint16_t*>(U.bl);
         int k = off;
@@ -244,23 +298,23 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
             U.gst[l] = 0u;
         }
     }
-    for (int i = lane; i < (N * N + 1) / 2; i += 32)
+    for (int i = r; i < (N * N + 1) / 2; i += L)
         reinterpret_cast<uint4*>(S.capx)[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncwarp();
+    g.sync();
     // liberty OR-stats per chain
-    for (int i = lane; i < total; i += 32) {
+    for (int i = r; i < total; i += L) {
         const uint32_t x = U.root[i];
         const uint32_t e = U.run[i];
         const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
         const uint32_t run = ((1u << len) - 1u) << s;
-        const uint32_t up = rr > 0 ? run & S.rE[rr - 1] : 0u, dn = run & S.rE[rr + 1];
+        const uint32_t up = rr > 0 ? run & S.rE[rr - 1] : 0u, dn = rr < N - 1 ? run & S.rE[rr + 1] : 0u;
         const uint32_t sd = ((run << 1) | (run >> 1)) & S.rE[rr];
         if (!(up | dn | sd)) continue;
         const uint32_t lo = up ? (rr - 1) * N + __ffs(up) - 1 : sd ? rr * N + __ffs(sd) - 1 : (rr + 1) * N + __ffs(dn) - 1;
         const uint32_t hi = dn ? (rr + 1) * N + 31 - __clz(dn) : sd ? rr * N + 31 - __clz(sd) : (rr - 1) * N + 31 - __clz(up);
         atomicOr(&U.gst[x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
-    __syncwarp();
+    g.sync();
     // the labels are dead now: async-copy this env's Bloom + pair filter over them, overlapped
     // with the classification pass (it includes the hash appended by this step)
     const uint32_t* bl = U.bl;
@@ -268,17 +322,17 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         __threadfence_block();
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(U.bl);
         const char* src = reinterpret_cast<const char*>(gbloom);
-        for (int i = lane; i < filter_words(N) / 4; i += 32)
+        for (int i = r; i < filter_words(N) / 4; i += L)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
         asm volatile("cp.async.commit_group;");
     }
     // 3. atari classification; capture liberties (+ zobrist XOR) of opponent atari groups
-    for (int i = lane; i < total; i += 32) {
-        const uint32_t g = U.gst[U.root[i]];
-        const bool at = !(g & 0x80000000u) || (g & (g >> 10) & 0x3FFu) == 0u;
+    for (int i = r; i < total; i += L) {
+        const uint32_t gs = U.gst[U.root[i]];
+        const bool at = !(gs & 0x80000000u) || (gs & (gs >> 10) & 0x3FFu) == 0u;
         const uint32_t e = U.run[i];
-        if ((e >> 15) && at && (g & 0x80000000u)) {
-            const uint32_t lib = g & 0x3FFu;
+        if ((e >> 15) && at && (gs & 0x80000000u)) {
+            const uint32_t lib = gs & 0x3FFu;
             atomicOr(&S.rcap[lib / N], 1u << (lib % N));
             const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
             uint64_t x = 0ull;
@@ -290,21 +344,21 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
+    g.sync();
     // NA: mover stones whose group has >= 2 liberties (this row's X runs)
     uint32_t NA = 0u;
     {
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++)
         {
-            const uint32_t g = U.gst[U.root[k]];
-            if ((g & (g >> 10) & 0x3FFu) != 0u) NA |= run_at(X, __ffs(s_) - 1);   // >= 2 liberties
+            const uint32_t gs = U.gst[U.root[k]];
+            if ((gs & (gs >> 10) & 0x3FFu) != 0u) NA |= run_at(X, __ffs(s_) - 1);   // >= 2 liberties
         }
     }
     // 5. candidates + superko filter (row-parallel)
-    const uint32_t Eu = up_row(E, lane), Ed = dn_row(E, lane);
-    const uint32_t capb = lane < N ? S.rcap[lane] : 0u;
-    const uint32_t NAu = up_row(NA, lane), NAd = dn_row(NA, lane);
+    const uint32_t Eu = g.up_row(E), Ed = g.dn_row(E);
+    const uint32_t capb = r < N ? S.rcap[r] : 0u;
+    const uint32_t NAu = g.up_row(NA), NAd = g.dn_row(NA);
     const uint32_t nb = ((E << 1) | (E >> 1) | Eu | Ed | (NA << 1) | (NA >> 1) | NAu | NAd) & ROW;
     uint32_t cand = E & (capb | nb);
     // Self-capture (go.py:155-173): an empty point whose own neighbours are all in atari on it
@@ -313,18 +367,18 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
     // it is not a capture point). A lone stone would recreate h itself: superko rejects it.
     uint32_t sc = 0u;
     if (self_capture) {
-        const uint32_t Xn = ((X << 1) | (X >> 1) | up_row(X, lane) | dn_row(X, lane)) & ROW;
+        const uint32_t Xn = ((X << 1) | (X >> 1) | g.up_row(X) | g.dn_row(X)) & ROW;
         sc = E & ~capb & ~nb & Xn;
-        if (__any_sync(BBK_FULL, sc != 0u)) {
-            __syncwarp();
-            S.rcap[lane] = sc;
-            __syncwarp();
-            for (int i = lane; i < total; i += 32) {
+        if (g.any(sc != 0u)) {
+            g.sync();
+            S.rcap[r] = sc;
+            g.sync();
+            for (int i = r; i < total; i += L) {
                 const uint32_t e = U.run[i];
                 if (e >> 15) continue;   // mover's runs only
-                const uint32_t g = U.gst[U.root[i]];
-                if ((g & (g >> 10) & 0x3FFu) != 0u) continue;   // >= 2 liberties
-                const uint32_t lib = g & 0x3FFu;
+                const uint32_t gs = U.gst[U.root[i]];
+                if ((gs & (gs >> 10) & 0x3FFu) != 0u) continue;   // >= 2 liberties
+                const uint32_t lib = gs & 0x3FFu;
                 if (!((S.rcap[lib / N] >> (lib % N)) & 1u)) continue;
                 const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
                 uint64_t x = 0ull;
@@ -333,7 +387,7 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
                 atomicXor(cx, (uint32_t)x);
                 atomicXor(cx + 1, (uint32_t)(x >> 32));
             }
-            __syncwarp();
+            g.sync();
         }
     }
     uint32_t legal = 0u, pend = 0u;
@@ -358,31 +412,31 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
         if (bloom_maybe<N>(bl, h2)) pend |= 1u << p;
         else legal |= 1u << p;
     }
-    while (__any_sync(BBK_FULL, pend != 0u)) {
-        const unsigned active = __ballot_sync(BBK_FULL, pend != 0u);
+    while (g.any(pend != 0u)) {
+        const unsigned active = g.ballot(pend != 0u);
         int p = pend ? __ffs(pend) - 1 : 0;
         uint64_t h2 = 0ull;
         if (pend) {
             int cell = r * N + p;
             h2 = ((sc >> p) & 1u) ? h : h ^ zkey<N>(cell, 1 - ycol);
             if (((capb | sc) >> p) & 1u) h2 ^= S.capx[cell];
-            S.u.sk.hit[lane] = h2;
+            S.u.sk.hit[r] = h2;
         }
-        __syncwarp();
+        g.sync();
         unsigned found = 0u;
-        for (int j = lane; j < nscan + 1; j += 32) {
+        for (int j = r; j < nscan + 1; j += L) {
             uint64_t v = j < nscan ? hist[j] : extra;
             for (unsigned a_ = active; a_; a_ &= a_ - 1) {
                 int l = __ffs(a_) - 1;
                 if (v == S.u.sk.hit[l]) found |= 1u << l;
             }
         }
-        found = __reduce_or_sync(BBK_FULL, found);
+        found = g.reduce_or(found);
         if (pend) {
-            if (!((found >> lane) & 1u)) legal |= 1u << p;
+            if (!((found >> r) & 1u)) legal |= 1u << p;
             pend &= pend - 1u;
         }
-        __syncwarp();
+        g.sync();
     }
     return legal;
 }
@@ -392,14 +446,15 @@ __device__ uint32_t legal_rows(WarpSmem<N>& S, int ycol, uint32_t X, uint32_t Y,
 // f % 17 of the point pattern P[f / 17]; the [N, N, 17] record is emitted as
 // float4 chunks of the flat 16-byte-aligned stream (records are not 16-B
 // aligned; at most 3 scalar floats at each edge) through a 16-entry LUT.
-template <int N>
-__device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t b, int role, int lane) {
+template <int N, int L>
+__device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, float* obs, int64_t b, int role) {
     constexpr int C = N * N;
     constexpr int NF = C * kPlanes;
+    const int sl = g.sl;
     uint32_t* P = S.u.ob.P;
     {   // 8 points per lane-iteration: black/white swapped for role 1, colour bit 16
         const uint32_t hi = (uint32_t)role << 16;
-        for (int i = lane; i < pat_stride(N) / 8; i += 32) {
+        for (int i = sl; i < pat_stride(N) / 8; i += L) {
             const uint4 v = reinterpret_cast<const uint4*>(S.pat)[i];
             auto sw = [&](uint32_t u) { return role ? (((u & 0x55555555u) << 1) | ((u >> 1) & 0x55555555u)) : u; };
             const uint32_t a = sw(v.x), bb = sw(v.y), c = sw(v.z), d = sw(v.w);
@@ -408,36 +463,59 @@ __device__ void emit_obs(WarpSmem<N>& S, const float4* lut, float* obs, int64_t 
             P4[1] = make_uint4((c & 0xFFFFu) | hi, (c >> 16) | hi, (d & 0xFFFFu) | hi, (d >> 16) | hi);
         }
     }
-    __syncwarp();
+    g.sync();
     // the record as a bit stream: bit f of W = float f (17 bits per point)
     uint32_t* W = S.u.ob.W;
     constexpr int NW = (NF + 31) / 32;
-    for (int w = lane; w < NW; w += 32) {
+    for (int w = sl; w < NW; w += L) {
         const uint32_t q = 32u * w, c = (q * 61681u) >> 20, k = q - 17u * c;   // q / 17, exact for q < 65536
         uint32_t v = (P[c] >> k) | (P[c + 1] << (17 - k));
         if (k > 2) v |= P[c + 2] << (34 - k);
         W[w] = v;
     }
-    if (lane == 0) W[NW] = 0u;
-    __syncwarp();
+    if (sl == 0) W[NW] = 0u;
+    g.sync();
     const int64_t F0 = b * (int64_t)NF;
     const int head = (int)((4 - (F0 & 3)) & 3);             // floats before the first aligned chunk
     const int nchunk = (NF - head) >> 2;
     float* rec = obs + F0;
     const int tail0 = head + 4 * nchunk;
-    if (lane < head || (lane >= 4 && lane - 4 < NF - tail0)) {
-        const uint32_t fi = lane < 4 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 4);
+    if (sl < head || (sl >= 4 && sl - 4 < NF - tail0)) {
+        const uint32_t fi = sl < 4 ? (uint32_t)sl : (uint32_t)(tail0 + sl - 4);
         rec[fi] = (float)((W[fi >> 5] >> (fi & 31)) & 1u);
     }
-    // chunk j = lane + 32 m starts at bit head + 4 lane + 128 m: a lane-constant bit
-    // offset in word (head + 4 lane) / 32 + 4 m
+    // chunk j = sl + L m starts at bit head + 4 sl + 4 L m: a lane-constant bit offset in
+    // word (head + 4 sl) / 32 + (L / 8) m
     float4* o4 = reinterpret_cast<float4*>(rec + head);
-    const uint32_t q0 = (uint32_t)(head + 4 * lane), sh = q0 & 31u;
+    const uint32_t q0 = (uint32_t)(head + 4 * sl), sh = q0 & 31u;
     const uint32_t* wp = W + (q0 >> 5);
 #pragma unroll 4
-    for (int j = lane; j < nchunk; j += 32, wp += 4)
+    for (int j = sl; j < nchunk; j += L, wp += L / 8)
         o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
-    __syncwarp();
+    g.sync();
+}
+
+// Write NBYTES bytes of a per-env record into a flat [n, NBYTES] byte stream from shared memory
+// staged at the destination's 16-byte phase (common.cuh warp_emit_bytes over the segment's lanes).
+template <int L>
+__device__ __forceinline__ void seg_emit_bytes(const Seg<L>& g, uint8_t* dst_stream, int64_t rec_start, int nbytes,
+                                               const uint8_t* staged) {
+    if constexpr (L == 32) {
+        warp_emit_bytes(dst_stream, rec_start, nbytes, staged);
+    } else {
+        const int64_t end = rec_start + nbytes;
+        const int64_t base = rec_start & ~(int64_t)15;
+        const int64_t f0 = (rec_start + 15) >> 4, f1 = end >> 4;
+        for (int64_t c = f0 + g.sl; c < f1; c += L)
+            *reinterpret_cast<uint4*>(dst_stream + (c << 4)) = *reinterpret_cast<const uint4*>(staged + ((c << 4) - base));
+        const int64_t head_end = (f0 << 4) < end ? (f0 << 4) : end;
+        {   // lane k: byte k of the partial head chunk, then byte k of the partial tail chunk
+            const int64_t gh = rec_start + g.sl;
+            if (g.sl < 16 && gh < head_end) dst_stream[gh] = staged[gh - base];
+            const int64_t gt = (f1 << 4) + g.sl;
+            if (g.sl < 16 && gt < end && gt >= (f0 << 4)) dst_stream[gt] = staged[gt - base];
+        }
+    }
 }
 
 // One scalar column of board b per lane (lanes 0-9), loaded a board ahead so the
@@ -478,8 +556,6 @@ __device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
     }
 }
 
-
-
 template <int N>
 __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
     if (threadIdx.x < 16) {
@@ -497,37 +573,39 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     constexpr int C = N * N;
     constexpr int A = C + 1;
     constexpr int PS = pat_stride(N);
+    constexpr int L = seg_lanes(N);
     constexpr uint32_t ROW = (1u << N) - 1u;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlockSmem<N>& B = *reinterpret_cast<BlockSmem<N>*>(smem_raw);
     init_block<N>(B);
-    const int lane = lane_id();
-    WarpSmem<N>& S = B.w[threadIdx.x >> 5];
-    const uint32_t rowm = lane < N ? ROW : 0u;
-    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    const Seg<L> g;
+    const int sl = g.sl;
+    WarpSmem<N>& S = B.w[threadIdx.x / L];
+    const uint32_t rowm = sl < N ? ROW : 0u;
+    const int64_t nboards = (int64_t)gridDim.x * boards_per_cta(N);   // boards in flight (grid stride)
     unsigned long long eps = 0;
     // next-board prefetch: scalar columns in registers (lane j holds field j), `pat` via
     // cp.async into an idle tail of the scratch union (not touched by mask/obs emission)
     uint16_t* pat_pf = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(&S.u) + pf_off(N));
     uint16_t* lab_pf = pat_pf + PS;
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
-    const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const FieldRefWide fref = widen(field_ref(p, lane), p.in.terminated);
+    const int64_t b0 = (int64_t)blockIdx.x * boards_per_cta(N) + threadIdx.x / L;
+    const FieldRefWide fref = widen(field_ref(p, sl), p.in.terminated);
     uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(fref, b0) : 0ull;
     bool pat_ready = false;
 
-    for (int64_t b = b0; b < p.n; b += nwarps) {
-        if (!p.force_reset && b + nwarps < p.n && lane < (4 * filter_words(N) + 127) / 128) {
+    for (int64_t b = b0; b < p.n; b += nboards) {
+        if (!p.force_reset && b + nboards < p.n && sl < (4 * filter_words(N) + 127) / 128) {
             // warm L2 with the next board's Bloom filter (cp.async'd mid-board)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                reinterpret_cast<const char*>(p.store.bloom + (b + nwarps) * (int64_t)filter_words(N)) + 128 * lane));
+                reinterpret_cast<const char*>(p.store.bloom + (b + nboards) * (int64_t)filter_words(N)) + 128 * sl));
         }
-        const uint64_t f_term = __shfl_sync(BBK_FULL, (uint32_t)pf, 0), f_trunc = __shfl_sync(BBK_FULL, (uint32_t)pf, 1);
-        const uint32_t f_p2r = __shfl_sync(BBK_FULL, (uint32_t)pf, 2), f_role = __shfl_sync(BBK_FULL, (uint32_t)pf, 3);
-        const uint32_t f_pass = __shfl_sync(BBK_FULL, (uint32_t)pf, 4), f_step = __shfl_sync(BBK_FULL, (uint32_t)pf, 5);
-        const uint64_t f_hash = shfl64(pf, 6), f_hx = shfl64(pf, 7);
-        const uint32_t f_hlen = __shfl_sync(BBK_FULL, (uint32_t)pf, 8);
-        const int64_t f_act = (int64_t)shfl64(pf, 9);
+        const uint64_t f_term = g.shfl((uint32_t)pf, 0), f_trunc = g.shfl((uint32_t)pf, 1);
+        const uint32_t f_p2r = g.shfl((uint32_t)pf, 2), f_role = g.shfl((uint32_t)pf, 3);
+        const uint32_t f_pass = g.shfl((uint32_t)pf, 4), f_step = g.shfl((uint32_t)pf, 5);
+        const uint64_t f_hash = g.shfl64(pf, 6), f_hx = g.shfl64(pf, 7);
+        const uint32_t f_hlen = g.shfl((uint32_t)pf, 8);
+        const int64_t f_act = (int64_t)g.shfl64(pf, 9);
         const bool reset = p.force_reset || f_term || f_trunc;
         const uint64_t k = slot_key(p.slot_keys, p.key, p.slot0, b);
         uint64_t* hist = p.store.history + b * (int64_t)p.store.hist_cap;
@@ -548,11 +626,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             role = 0; pass_count = 0; step = 0; h = 0ull; hx = 0ull; hlen = 1;
             // the discarded prefetch of this board must land before the scratch is reused
             if (pat_ready) asm volatile("cp.async.wait_all;" ::: "memory");
-            for (int i = lane; i < PS; i += 32) { S.pat[i] = 0; lab[i] = 0; }
-            for (int i = lane; i < filter_words(N) / 4; i += 32)
+            for (int i = sl; i < PS; i += L) { S.pat[i] = 0; lab[i] = 0; }
+            for (int i = sl; i < filter_words(N) / 4; i += L)
                 reinterpret_cast<uint4*>(gbloom)[i] = make_uint4(0u, 0u, 0u, 0u);
-            __syncwarp();
-            if (lane == 0) { bloom_add<N>(gbloom, 0ull); pair_add<N>(gbloom, 0, 0); hist[0] = 0ull; }
+            g.sync();
+            if (sl == 0) { bloom_add<N>(gbloom, 0ull); pair_add<N>(gbloom, 0, 0); hist[0] = 0ull; }
             nscan = 0; extra = 0ull;
         } else {
             p2r0 = (int8_t)(f_p2r & 0xFF); p2r1 = (int8_t)(f_p2r >> 8);
@@ -574,31 +652,31 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             };
             if (pat_ready) {   // prefetched during the previous board
                 asm volatile("cp.async.wait_all;" ::: "memory");
-                __syncwarp();
-                for (int i = lane; i < PS / 8; i += 32) {
+                g.sync();
+                for (int i = sl; i < PS / 8; i += L) {
                     take(i, reinterpret_cast<const uint4*>(pat_pf)[i]);
                     reinterpret_cast<uint4*>(lab)[i] = reinterpret_cast<const uint4*>(lab_pf)[i];
                 }
             } else {
                 const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
                 const uint4* lsrc = reinterpret_cast<const uint4*>(p.in_s.lab + b * (int64_t)PS);
-                for (int i = lane; i < PS / 8; i += 32) {
+                for (int i = sl; i < PS / 8; i += L) {
                     take(i, src[i]);
                     reinterpret_cast<uint4*>(lab)[i] = lsrc[i];
                 }
             }
-            __syncwarp();
+            g.sync();
             if constexpr (N > 13) {
-                if (lane < N) {
+                if (sl < N) {
 #pragma unroll 4
                     for (int col = 0; col < N; col++) {
-                        uint32_t v = S.pat[lane * N + col];
+                        uint32_t v = S.pat[sl * N + col];
                         Bk |= (v & 1u) << col;
                         Wh |= ((v >> 1) & 1u) << col;
                     }
                 }
-            } else if (lane < N) {
-                const int q = lane * N, w = q >> 5, sh = q & 31;
+            } else if (sl < N) {
+                const int q = sl * N, w = q >> 5, sh = q & 31;
                 const uint32_t* fb = reinterpret_cast<const uint32_t*>(FB);
                 const uint32_t* fw = reinterpret_cast<const uint32_t*>(FW);
                 Bk = __funnelshift_r(fb[w], fb[w + 1], sh) & ROW;
@@ -611,33 +689,33 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 pass_count += 1;
                 if (pass_count == 2) {
                     terminal = true;
-                    score<N>(Bk, Wh, p.komi, lane, rr0, rr1);
+                    score<N>(g, Bk, Wh, p.komi, rr0, rr1);
                 }
             } else {                 // placement (go.py:232-262)
                 const int ra = a / N, ca = a - ra * N;
                 uint32_t M = role == 0 ? Bk : Wh, O = role == 0 ? Wh : Bk;
                 {   // chain label of the new stone: the first own neighbour's, absorbing the others
-                    const uint32_t Mr = __shfl_sync(BBK_FULL, M, ra);
-                    const uint32_t Mu = __shfl_sync(BBK_FULL, M, ra > 0 ? ra - 1 : 0);
-                    const uint32_t Md = __shfl_sync(BBK_FULL, M, ra < N - 1 ? ra + 1 : 0);
+                    const uint32_t Mr = g.shfl(M, ra);
+                    const uint32_t Mu = g.shfl(M, ra > 0 ? ra - 1 : 0);
+                    const uint32_t Md = g.shfl(M, ra < N - 1 ? ra + 1 : 0);
                     constexpr uint32_t NONE = 0xFFFFu;   // never a label (labels < C)
                     const uint32_t lu = (ra > 0 && ((Mu >> ca) & 1u)) ? lab[a - N] : NONE;
                     const uint32_t ld = (ra < N - 1 && ((Md >> ca) & 1u)) ? lab[a + N] : NONE;
                     const uint32_t ll = (ca > 0 && ((Mr >> (ca - 1)) & 1u)) ? lab[a - 1] : NONE;
                     const uint32_t lr = (ca < N - 1 && ((Mr >> (ca + 1)) & 1u)) ? lab[a + 1] : NONE;
                     const uint32_t L0 = lu != NONE ? lu : ld != NONE ? ld : ll != NONE ? ll : lr != NONE ? lr : (uint32_t)a;
-                    __syncwarp();
+                    g.sync();
                     if ((ld != NONE && ld != L0) | (ll != NONE && ll != L0) | (lr != NONE && lr != L0)) {
                         for (uint32_t m_ = M; m_; m_ &= m_ - 1) {   // lanes >= N hold no stones
-                            const int cell = lane * N + __ffs(m_) - 1;
+                            const int cell = sl * N + __ffs(m_) - 1;
                             const uint32_t l = lab[cell];
                             if (l == ld || l == ll || l == lr) lab[cell] = (uint16_t)L0;
                         }
                     }
-                    if (lane == 0) lab[a] = (uint16_t)L0;
-                    __syncwarp();
+                    if (sl == 0) lab[a] = (uint16_t)L0;
+                    g.sync();
                 }
-                if (lane == ra) M |= 1u << ca;
+                if (sl == ra) M |= 1u << ca;
                 const uint32_t E0 = ~(M | O) & rowm;
                 uint64_t capxor = 0ull;
                 uint32_t visited = 0u, dead = 0u;
@@ -647,46 +725,46 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 for (int j = 0; j < 4; j++) {
                     const int qr = qr_[j], qc = qc_[j];
                     if (qr < 0 || qr >= N || qc < 0 || qc >= N) continue;
-                    const uint32_t Oq = __shfl_sync(BBK_FULL, O, qr);
-                    const uint32_t Vq = __shfl_sync(BBK_FULL, visited, qr);
+                    const uint32_t Oq = g.shfl(O, qr);
+                    const uint32_t Vq = g.shfl(visited, qr);
                     if (!((Oq >> qc) & 1u) || ((Vq >> qc) & 1u)) continue;
                     // quick exit: the stone itself touches an empty point
-                    const uint32_t Er = __shfl_sync(BBK_FULL, E0, qr);
-                    const uint32_t Eup = qr > 0 ? __shfl_sync(BBK_FULL, E0, qr - 1) : 0u;
-                    const uint32_t Edn = qr < N - 1 ? __shfl_sync(BBK_FULL, E0, qr + 1) : 0u;
+                    const uint32_t Er = g.shfl(E0, qr);
+                    const uint32_t Eup = qr > 0 ? g.shfl(E0, qr - 1) : 0u;
+                    const uint32_t Edn = qr < N - 1 ? g.shfl(E0, qr + 1) : 0u;
                     if ((((Er << 1) | (Er >> 1) | Eup | Edn) >> qc) & 1u) continue;
-                    uint32_t F = lane == qr ? (1u << qc) : 0u;
+                    uint32_t F = sl == qr ? (1u << qc) : 0u;
                     while (true) {
-                        uint32_t F2 = (F | dilate<N>(F, lane)) & O;
-                        bool ch = __any_sync(BBK_FULL, F2 != F);
+                        uint32_t F2 = (F | dilate<N>(g, F)) & O;
+                        bool ch = g.any(F2 != F);
                         F = F2;
                         if (!ch) break;
                     }
                     visited |= F;
-                    if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E0) != 0u)) dead |= F;
+                    if (!g.any((dilate<N>(g, F) & E0) != 0u)) dead |= F;
                 }
-                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zkey<N>(lane * N + __ffs(d_) - 1, 1 - role);
+                for (uint32_t d_ = dead; d_; d_ &= d_ - 1) capxor ^= zkey<N>(sl * N + __ffs(d_) - 1, 1 - role);
                 O &= ~dead;
-                if (p.self_capture && !__any_sync(BBK_FULL, dead != 0u)) {
+                if (p.self_capture && !g.any(dead != 0u)) {
                     // go.py:249-255: the placed stone's group without a liberty is removed
-                    uint32_t F = lane == ra ? (1u << ca) : 0u;
+                    uint32_t F = sl == ra ? (1u << ca) : 0u;
                     while (true) {
-                        const uint32_t F2 = (F | dilate<N>(F, lane)) & M;
-                        const bool ch = __any_sync(BBK_FULL, F2 != F);
+                        const uint32_t F2 = (F | dilate<N>(g, F)) & M;
+                        const bool ch = g.any(F2 != F);
                         F = F2;
                         if (!ch) break;
                     }
                     const uint32_t E1 = ~(M | O) & rowm;
-                    if (!__any_sync(BBK_FULL, (dilate<N>(F, lane) & E1) != 0u)) {
-                        for (uint32_t f_ = F; f_; f_ &= f_ - 1) capxor ^= zkey<N>(lane * N + __ffs(f_) - 1, role);
+                    if (!g.any((dilate<N>(g, F) & E1) != 0u)) {
+                        for (uint32_t f_ = F; f_; f_ &= f_ - 1) capxor ^= zkey<N>(sl * N + __ffs(f_) - 1, role);
                         M &= ~F;
                     }
                 }
-                const uint64_t h2 = h ^ zkey<N>(a, role) ^ warp_xor64(capxor);
+                const uint64_t h2 = h ^ zkey<N>(a, role) ^ g.xor64(capxor);
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
-                counts = warp_sum(__popc(Bk) | (__popc(Wh) << 16));
+                counts = g.sum(__popc(Bk) | (__popc(Wh) << 16));
                 const int nbk = counts & 0xFFFF, nwh = counts >> 16;
-                if (lane == 0) {
+                if (sl == 0) {
                     hist[hlen] = h2;
                     bloom_add<N>(gbloom, h2);
                     pair_add<N>(gbloom, nbk, nwh);
@@ -699,26 +777,26 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         // new transposed history: pat' = pat << 2 | current board (go.py:224, 260)
         uint16_t* opat = p.out_s.pat + b * (int64_t)PS;
         if constexpr (N > 13) {   // row-parallel: this lane's row bits are in registers
-            if (!reset && lane < N) {
+            if (!reset && sl < N) {
 #pragma unroll 4
                 for (int col = 0; col < N; col++) {
-                    const int i = lane * N + col;
+                    const int i = sl * N + col;
                     S.pat[i] = (uint16_t)(((uint32_t)S.pat[i] << 2) | ((Bk >> col) & 1u) | (((Wh >> col) & 1u) << 1));
                 }
             }
-        } else {                  // small boards: point-parallel over all 32 lanes
-            S.rX[lane] = Bk; S.rY[lane] = Wh;
-            __syncwarp();
+        } else {                  // small boards: point-parallel over all the segment's lanes
+            S.rX[sl] = Bk; S.rY[sl] = Wh;
+            g.sync();
             if (!reset) {
-                for (int i = lane; i < C; i += 32) {
+                for (int i = sl; i < C; i += L) {
                     const int rr = i / N, cc = i - rr * N;
                     S.pat[i] = (uint16_t)(((uint32_t)S.pat[i] << 2) | ((S.rX[rr] >> cc) & 1u) | (((S.rY[rr] >> cc) & 1u) << 1));
                 }
             }
         }
-        __syncwarp();
+        g.sync();
         uint16_t* olab = p.out_s.lab + b * (int64_t)PS;
-        for (int i = lane; i < PS / 8; i += 32) {
+        for (int i = sl; i < PS / 8; i += L) {
             reinterpret_cast<uint4*>(opat)[i] = reinterpret_cast<const uint4*>(S.pat)[i];
             reinterpret_cast<uint4*>(olab)[i] = reinterpret_cast<const uint4*>(lab)[i];
         }
@@ -728,30 +806,25 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         if (!terminal && !truncated) {
             const uint32_t X = role == 0 ? Bk : Wh, Y = role == 0 ? Wh : Bk;
             const uint32_t E = ~(Bk | Wh) & rowm;
-            if (counts < 0) counts = warp_sum(__popc(Bk) | (__popc(Wh) << 16));
+            if (counts < 0) counts = g.sum(__popc(Bk) | (__popc(Wh) << 16));
             const int nbk = counts & 0xFFFF, nwh = counts >> 16;
-            legal = legal_rows<N>(S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, p.self_capture != 0, lane);
+            legal = legal_rows<N>(g, S, 1 - role, X, Y, E, h, hist, gbloom, nscan, extra, nbk, nwh, p.self_capture != 0);
         }
-        __syncwarp();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
+        g.sync();   // the analysis scratch (atari flags, superko hits) is reused for mask staging
         // stage mask bytes at the destination's 16-byte phase and emit
         const int64_t mstart = b * (int64_t)A;
         const int moff = (int)(mstart & 15);
-        if (lane < N) {
-            for (int col = 0; col < N; col++) S.u.mb[moff + lane * N + col] = (uint8_t)((legal >> col) & 1u);
+        if (sl < N) {
+            for (int col = 0; col < N; col++) S.u.mb[moff + sl * N + col] = (uint8_t)((legal >> col) & 1u);
         }
-        if (lane == 0) S.u.mb[moff + C] = (uint8_t)(!terminal && !truncated);
-        __syncwarp();
-        warp_emit_bytes(p.out.legal_action_mask, mstart, A, S.u.mb);
+        if (sl == 0) S.u.mb[moff + C] = (uint8_t)(!terminal && !truncated);
+        g.sync();
+        seg_emit_bytes(g, p.out.legal_action_mask, mstart, A, S.u.mb);
         eps += (terminal || truncated) ? 1 : 0;
         if (p.out.next_actions) {   // fused agents.random_actions on the new mask (row bits + pass, still on chip)
             const int c = __popc(legal);
-            int incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(BBK_FULL, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const int cells = __shfl_sync(BBK_FULL, incl, 31);
+            const int incl = g.scan(c);
+            const int cells = g.shfl(incl, L - 1);
             const bool live = !terminal && !truncated;
             const int total = live ? cells + 1 : 0;   // + pass
             int64_t act = 0;
@@ -764,31 +837,31 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                     if (mine) {
                         uint32_t v = legal;
                         for (int r = d - (incl - c); r > 0; r--) v &= v - 1;
-                        pos = lane * N + __ffs(v) - 1;
+                        pos = sl * N + __ffs(v) - 1;
                     }
-                    const unsigned who = __ballot_sync(BBK_FULL, mine);
-                    act = __shfl_sync(BBK_FULL, pos, __ffs(who) - 1);
+                    const unsigned who = g.ballot(mine);
+                    act = g.shfl(pos, __ffs(who) - 1);
                 }
             }
-            if (lane == 0) p.out.next_actions[b] = act;
+            if (sl == 0) p.out.next_actions[b] = act;
         }
-        __syncwarp();   // staged mask bytes are overwritten by the observation pattern next
+        g.sync();   // staged mask bytes are overwritten by the observation pattern next
         pat_ready = false;
-        if (!p.force_reset && b + nwarps < p.n) {   // issue the next board's loads now
-            const int64_t nb = b + nwarps;
+        if (!p.force_reset && b + nboards < p.n) {   // issue the next board's loads now
+            const int64_t nb = b + nboards;
             pf = load_field(fref, nb);
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
             const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
             const char* lsrc = reinterpret_cast<const char*>(p.in_s.lab + nb * (int64_t)PS);
-            for (int i = lane; i < PS / 8; i += 32) {
+            for (int i = sl; i < PS / 8; i += L) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 2u * PS + 16u * i), "l"(lsrc + 16 * i));
             }
             asm volatile("cp.async.commit_group;");
             pat_ready = true;
         }
-        if (p.out.observation) emit_obs<N>(S, B.lut, p.out.observation, b, role, lane);
-        if (lane == 0) {
+        if (p.out.observation) emit_obs<N>(g, S, B.lut, p.out.observation, b, role);
+        if (sl == 0) {
             float r0 = 0.0f, r1 = 0.0f;
             if (!truncated && (rr0 != 0.0f || rr1 != 0.0f)) {   // core.py:197-204
                 r0 = p2r0 == 0 ? rr0 : rr1;
@@ -808,29 +881,28 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             p.out_s.role_to_move[b] = (uint8_t)role;
             p.out_s.pass_count[b] = (uint8_t)pass_count;
         }
-        __syncwarp();
+        g.sync();
     }
-    if (p.out.episodes && lane == 0 && eps) atomicAdd(p.out.episodes, eps);
+    // a cp.async issued for a board this lane never processes (none: the prefetch is only issued
+    // for b + nboards < n) -- nothing is left in flight here
+    if (p.out.episodes && sl == 0 && eps) atomicAdd(p.out.episodes, eps);
 }
 
 template <int N>
 __global__ void __launch_bounds__(kWarps * 32) observe_kernel(const uint16_t* pat, const uint8_t* role, float* obs, int64_t n) {
     constexpr int PS = pat_stride(N);
+    constexpr int L = seg_lanes(N);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlockSmem<N>& B = *reinterpret_cast<BlockSmem<N>*>(smem_raw);
-    if (threadIdx.x < 16) {
-        uint32_t q = threadIdx.x;
-        B.lut[q] = make_float4((float)(q & 1), (float)((q >> 1) & 1), (float)((q >> 2) & 1), (float)((q >> 3) & 1));
-    }
-    __syncthreads();
-    const int lane = lane_id();
-    WarpSmem<N>& S = B.w[threadIdx.x >> 5];
-    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < n; b += nwarps) {
+    init_block<N>(B);
+    const Seg<L> g;
+    WarpSmem<N>& S = B.w[threadIdx.x / L];
+    const int64_t nboards = (int64_t)gridDim.x * boards_per_cta(N);
+    for (int64_t b = (int64_t)blockIdx.x * boards_per_cta(N) + threadIdx.x / L; b < n; b += nboards) {
         const uint4* src = reinterpret_cast<const uint4*>(pat + b * (int64_t)PS);
-        for (int i = lane; i < PS / 8; i += 32) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
-        __syncwarp();
-        emit_obs<N>(S, B.lut, obs, b, role[b], lane);
+        for (int i = g.sl; i < PS / 8; i += L) reinterpret_cast<uint4*>(S.pat)[i] = src[i];
+        g.sync();
+        emit_obs<N>(g, S, B.lut, obs, b, role[b]);
     }
 }
 
@@ -898,7 +970,7 @@ static int launch_step(const StepParams& p, cudaStream_t stream) {
         per_sm_dev[dev] = per_sm < 1 ? 1 : per_sm;
     }
     const int per_sm = per_sm_dev[dev];
-    int64_t need = (p.n + kWarps - 1) / kWarps;
+    int64_t need = (p.n + boards_per_cta(N) - 1) / boards_per_cta(N);
     int64_t grid = (int64_t)num_sms() * per_sm;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
@@ -910,7 +982,7 @@ template <int N>
 static int launch_observe(const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, cudaStream_t stream) {
     const size_t smem = sizeof(BlockSmem<N>);
     cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int64_t need = (n + kWarps - 1) / kWarps;
+    int64_t need = (n + boards_per_cta(N) - 1) / boards_per_cta(N);
     int64_t grid = need < (int64_t)num_sms() * 4 ? need : (int64_t)num_sms() * 4;
     observe_kernel<N><<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, smem, stream>>>(pat, role, obs, n);
     return (int)cudaGetLastError();
