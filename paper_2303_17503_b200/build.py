@@ -53,7 +53,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+        # BBK_NVCC_EXTRA: extra nvcc flags for A/B builds of tuning variants (tools/variant.sh)
+        cmd = [nvcc(), *ARCH, *FLAGS, *os.environ.get("BBK_NVCC_EXTRA", "").split(), "-I", INCLUDE, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
