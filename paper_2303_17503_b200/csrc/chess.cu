@@ -267,7 +267,6 @@ __device__ int task_moves(const GenCtx& c, uint16_t tk, bool& ep_legal) {
         return cnt;
     }
     uint64_t allow = c.checkmask;
-#pragma unroll
     if ((c.pinned >> sq) & 1ull)   // the 8 pin slots are read only for a pinned piece
         for (int j = 0; j < 8; j++) if (c.pinsq[j] == sq) allow &= c.pinray[j];
     if (d < 8) {   // slider ray

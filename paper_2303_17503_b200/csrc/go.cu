@@ -561,11 +561,21 @@ __device__ __forceinline__ FieldRefWide widen(FieldRef f, const void* any) {
     return {reinterpret_cast<const char*>(f.v & ((1ull << 58) - 1ull)), lsz,
             lsz == 3u ? ~0ull : (1ull << (8u << lsz)) - 1ull};
 }
-__device__ __forceinline__ uint64_t load_field(const FieldRefWide& f, int64_t b) {
+// The raw aligned word and the element's bit offset: decoded (shift + mask) only when the board
+// is processed, so no instruction waits on the load while the current board is being finished.
+__device__ __forceinline__ uint64_t load_field_raw(const FieldRefWide& f, int64_t b, uint32_t& sh) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(f.base) + ((uintptr_t)b << f.lsz);
-    const uint64_t w = *reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
-    return (w >> (8u * (uint32_t)(a & 7u))) & f.mask;
+    sh = 8u * (uint32_t)(a & 7u);
+    return *reinterpret_cast<const uint64_t*>(a & ~(uintptr_t)7);
 }
+__device__ __forceinline__ uint64_t load_field(const FieldRefWide& f, int64_t b) {
+    uint32_t sh;
+    const uint64_t w = load_field_raw(f, b, sh);
+    return (w >> sh) & f.mask;
+}
+// deferred decode for the small boards (+1 % at 9x9); 19x19 decodes at the load (the extra live
+// register across the board cost 1.7 % there)
+template <int N> constexpr bool kDeferFields = N <= 13;
 
 __device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
     switch (lane) {
@@ -627,7 +637,12 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
     const int64_t b0 = (int64_t)blockIdx.x * boards_per_cta(N) + threadIdx.x / L;
     const FieldRefWide fref = widen(field_ref(p, sl), p.in.terminated);
-    uint64_t pf = (!p.force_reset && b0 < p.n) ? load_field(fref, b0) : 0ull;
+    uint32_t pf_sh = 0u;
+    uint64_t pf_raw = 0ull;
+    if (!p.force_reset && b0 < p.n) {
+        if constexpr (kDeferFields<N>) pf_raw = load_field_raw(fref, b0, pf_sh);
+        else pf_raw = load_field(fref, b0);
+    }
     bool pat_ready = false;
 
     for (int64_t b = b0; b < p.n; b += nboards) {
@@ -636,6 +651,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             asm volatile("prefetch.global.L2 [%0];" ::"l"(
                 reinterpret_cast<const char*>(p.store.bloom + (b + nboards) * (int64_t)filter_words(N)) + 128 * sl));
         }
+        const uint64_t pf = kDeferFields<N> ? (pf_raw >> pf_sh) & fref.mask : pf_raw;
         const uint64_t f_term = g.shfl((uint32_t)pf, 0), f_trunc = g.shfl((uint32_t)pf, 1);
         const uint32_t f_p2r = g.shfl((uint32_t)pf, 2), f_role = g.shfl((uint32_t)pf, 3);
         const uint32_t f_pass = g.shfl((uint32_t)pf, 4), f_step = g.shfl((uint32_t)pf, 5);
@@ -883,7 +899,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         pat_ready = false;
         if (!p.force_reset && b + nboards < p.n) {   // issue the next board's loads now
             const int64_t nb = b + nboards;
-            pf = load_field(fref, nb);
+            if constexpr (kDeferFields<N>) pf_raw = load_field_raw(fref, nb, pf_sh);
+            else pf_raw = load_field(fref, nb);
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
             const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
             const char* lsrc = reinterpret_cast<const char*>(p.in_s.lab + nb * (int64_t)PS);
