@@ -54,13 +54,6 @@ __host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v
 
 __host__ __device__ constexpr int pat_stride(int N) { return (N * N + 7) & ~7; }
 
-// byte offset of the next board's prefetched pat (then lab) inside the scratch union:
-// past the observation and mask scratch, which are live while the prefetch is in flight
-__host__ __device__ constexpr int pf_off(int N) {
-    const int ob = 4 * pat_stride(N) + 4 * ((N * N * 17 + 31) / 32 + 2), mb = (N * N + 1 + 47) & ~15;
-    return ((ob > mb ? ob : mb) + 15) & ~15;
-}
-
 // The lanes of one board: shuffles / votes / syncs over the segment's mask only (width L), so the
 // two boards of a split warp never wait on each other.
 template <int L>
@@ -126,7 +119,12 @@ struct WarpSmem {   // one board's scratch (one per segment)
     static constexpr int C = N * N;
     static constexpr int A = C + 1;
     static constexpr int L = seg_lanes(N);
-    static constexpr int MAXR = ((N + 1) / 2) * 2 * N + 32;   // >= max runs of both colours
+    static constexpr int MAXR = C;   // runs of both colours: each holds >= 1 stone
+    // Per point, live during the legal-mask analysis: at an empty point the XOR of the zobrist keys
+    // of the chains a stone there would capture; at a stone that is its chain's label, the chain's
+    // liberty stats OR(lib) | OR(~lib) << 10 | HAS in the low word (labels are stones, capture
+    // points are empty: the two never share a point). Between the analysis and the next board's
+    // start it is the landing zone of the next board's prefetched `pat` and `lab`.
     uint64_t capx[C];
     // Phase-multiplexed scratch (each member is dead before the next one is written):
     // chain labels -> group analysis -> superko hits -> staged mask bytes -> observation pattern.
@@ -137,7 +135,6 @@ struct WarpSmem {   // one board's scratch (one per segment)
             alignas(16) uint32_t bl[filter_words(N)];
             uint16_t run[MAXR];    // (colour << 15) | (row << 10) | (start << 5) | len
             uint16_t root[MAXR];   // chain label of the run
-            uint32_t gst[C];       // OR(lib) | OR(~lib) << 10 | HAS, by chain label
         } uf;
         struct {
             uint32_t bloom_area[filter_words(N)];
@@ -150,10 +147,11 @@ struct WarpSmem {   // one board's scratch (one per segment)
         } ob;
     } u;
     static_assert(2 * pat_stride(N) <= 4 * filter_words(N), "labels must fit the filter landing area");
-    static_assert(pf_off(N) + 4 * pat_stride(N) <= (int)sizeof(u), "pat + lab prefetch must fit the union");
+    static_assert(4 * pat_stride(N) <= 8 * C, "pat + lab prefetch must fit the capture-XOR array");
     static_assert(N <= L, "a board's rows must fit its lanes");
     alignas(16) uint16_t pat[pat_stride(N)];
-    uint32_t rX[L], rY[L], rE[L], rcap[L];   // rX/rY double as rowB/rowW and the flat stone bitmaps
+    // rX / rY: rows of black / white and the flat stone bitmaps (small boards only)
+    uint32_t rX[N <= 13 ? L : 1], rY[N <= 13 ? L : 1], rE[L], rcap[L];
     static_assert(L == 32 || 4 * L >= pat_stride(N) / 8 + 8, "flat stone bitmaps must fit rX / rY");
 };
 
@@ -308,7 +306,8 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
     int off = g.scan(cnt);   // inclusive prefix sum of run counts over rows
     const int total = g.shfl(off, L - 1);
     off -= cnt;
-    S.rX[r] = X; S.rY[r] = Y; S.rE[r] = E; S.rcap[r] = 0u;
+    S.rE[r] = E; S.rcap[r] = 0u;
+    uint32_t* gst = reinterpret_cast<uint32_t*>(S.capx);   // chain stats at 2 * label (see WarpSmem)
     {   // this row's runs -> list, each with its chain label
         const uint16_t* lab = reinterpret_cast<const uint16_t*>(U.bl);
         int k = off;
@@ -317,14 +316,12 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
             U.run[k] = (uint16_t)((0u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(X >> s)) - 1));
             const uint16_t l = lab[r * N + s];
             U.root[k] = l;
-            U.gst[l] = 0u;
         }
         for (uint32_t s_ = SY; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
             U.run[k] = (uint16_t)((1u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(Y >> s)) - 1));
             const uint16_t l = lab[r * N + s];
             U.root[k] = l;
-            U.gst[l] = 0u;
         }
     }
     for (int i = r; i < (N * N + 1) / 2; i += L)
@@ -341,7 +338,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         if (!(up | dn | sd)) continue;
         const uint32_t lo = up ? (rr - 1) * N + __ffs(up) - 1 : sd ? rr * N + __ffs(sd) - 1 : (rr + 1) * N + __ffs(dn) - 1;
         const uint32_t hi = dn ? (rr + 1) * N + 31 - __clz(dn) : sd ? rr * N + 31 - __clz(sd) : (rr - 1) * N + 31 - __clz(up);
-        atomicOr(&U.gst[x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
+        atomicOr(&gst[2 * x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
     }
     g.sync();
     // the labels are dead now: async-copy this env's Bloom + pair filter over them, overlapped
@@ -357,7 +354,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
     }
     // 3. atari classification; capture liberties (+ zobrist XOR) of opponent atari groups
     for (int i = r; i < total; i += L) {
-        const uint32_t gs = U.gst[U.root[i]];
+        const uint32_t gs = gst[2 * U.root[i]];
         const bool at = !(gs & 0x80000000u) || (gs & (gs >> 10) & 0x3FFu) == 0u;
         const uint32_t e = U.run[i];
         if ((e >> 15) && at && (gs & 0x80000000u)) {
@@ -379,7 +376,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++)
         {
-            const uint32_t gs = U.gst[U.root[k]];
+            const uint32_t gs = gst[2 * U.root[k]];
             if ((gs & (gs >> 10) & 0x3FFu) != 0u) NA |= run_at(X, __ffs(s_) - 1);   // >= 2 liberties
         }
     }
@@ -404,7 +401,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
             for (int i = r; i < total; i += L) {
                 const uint32_t e = U.run[i];
                 if (e >> 15) continue;   // mover's runs only
-                const uint32_t gs = U.gst[U.root[i]];
+                const uint32_t gs = gst[2 * U.root[i]];
                 if ((gs & (gs >> 10) & 0x3FFu) != 0u) continue;   // >= 2 liberties
                 const uint32_t lib = gs & 0x3FFu;
                 if (!((S.rcap[lib / N] >> (lib % N)) & 1u)) continue;
@@ -516,6 +513,8 @@ __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, flo
     float4* o4 = reinterpret_cast<float4*>(rec + head);
     const uint32_t q0 = (uint32_t)(head + 4 * sl), sh = q0 & 31u;
     const uint32_t* wp = W + (q0 >> 5);
+    // (an ALU expansion of the 4 bits -- (t & 2^k) * (0x3F800000 >> k) -- instead of the LUT measured
+    // -0.2 % at 19x19 and -1 % at 9x9 in r02, although the L1 / shared pipe is the busiest unit)
 #pragma unroll 4
     for (int j = sl; j < nchunk; j += L, wp += L / 8)
         o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
@@ -612,7 +611,10 @@ constexpr int kNbUnroll = BBK_GO_NB_UNROLL;
 #ifndef BBK_GO_CTAS_SMALL
 #define BBK_GO_CTAS_SMALL 8
 #endif
-__host__ __device__ constexpr int min_ctas(int N) { return N <= 13 ? BBK_GO_CTAS_SMALL : 6; }
+#ifndef BBK_GO_CTAS_LARGE
+#define BBK_GO_CTAS_LARGE 6
+#endif
+__host__ __device__ constexpr int min_ctas(int N) { return N <= 13 ? BBK_GO_CTAS_SMALL : BBK_GO_CTAS_LARGE; }
 
 template <int N>
 __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepParams p) {
@@ -632,7 +634,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     unsigned long long eps = 0;
     // next-board prefetch: scalar columns in registers (lane j holds field j), `pat` via
     // cp.async into an idle tail of the scratch union (not touched by mask/obs emission)
-    uint16_t* pat_pf = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(&S.u) + pf_off(N));
+    uint16_t* pat_pf = reinterpret_cast<uint16_t*>(S.capx);   // dead from the mask on (see WarpSmem)
     uint16_t* lab_pf = pat_pf + PS;
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
     const int64_t b0 = (int64_t)blockIdx.x * boards_per_cta(N) + threadIdx.x / L;
