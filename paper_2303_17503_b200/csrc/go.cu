@@ -500,24 +500,51 @@ __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, flo
     if (sl == 0) W[NW] = 0u;
     g.sync();
     const int64_t F0 = b * (int64_t)NF;
-    const int head = (int)((4 - (F0 & 3)) & 3);             // floats before the first aligned chunk
-    const int nchunk = (NF - head) >> 2;
     float* rec = obs + F0;
-    const int tail0 = head + 4 * nchunk;
-    if (sl < head || (sl >= 4 && sl - 4 < NF - tail0)) {
-        const uint32_t fi = sl < 4 ? (uint32_t)sl : (uint32_t)(tail0 + sl - 4);
-        rec[fi] = (float)((W[fi >> 5] >> (fi & 31)) & 1u);
-    }
-    // chunk j = sl + L m starts at bit head + 4 sl + 4 L m: a lane-constant bit offset in
-    // word (head + 4 sl) / 32 + (L / 8) m
-    float4* o4 = reinterpret_cast<float4*>(rec + head);
-    const uint32_t q0 = (uint32_t)(head + 4 * sl), sh = q0 & 31u;
-    const uint32_t* wp = W + (q0 >> 5);
-    // (an ALU expansion of the 4 bits -- (t & 2^k) * (0x3F800000 >> k) -- instead of the LUT measured
-    // -0.2 % at 19x19 and -1 % at 9x9 in r02, although the L1 / shared pipe is the busiest unit)
+#ifndef BBK_GO_OBS_V8
+#define BBK_GO_OBS_V8 1
+#endif
+    if constexpr (BBK_GO_OBS_V8) {
+        // 32-byte stores (st.global.v8.f32): a warp writing whole per-board records absorbs 6.1-6.2
+        // TB/s this way against 5.3-5.5 TB/s with 16-byte stores (tools/write_pattern.cu, B200)
+        const int head = (int)((8 - (F0 & 7)) & 7);             // floats before the first 32-B chunk
+        const int nchunk = (NF - head) >> 3;
+        const int tail0 = head + 8 * nchunk;
+        if (sl < head || (sl >= 8 && sl - 8 < NF - tail0)) {   // at most 7 edge floats each side
+            const uint32_t fi = sl < 8 ? (uint32_t)sl : (uint32_t)(tail0 + sl - 8);
+            rec[fi] = (float)((W[fi >> 5] >> (fi & 31)) & 1u);
+        }
+        // chunk j = sl + L m starts at bit head + 8 sl + 8 L m: a lane-constant bit offset in
+        // word (head + 8 sl) / 32 + (L / 4) m
+        float* o8 = rec + head;
+        const uint32_t q0 = (uint32_t)(head + 8 * sl), sh = q0 & 31u;
+        const uint32_t* wp = W + (q0 >> 5);
+#pragma unroll 2
+        for (int j = sl; j < nchunk; j += L, wp += L / 4) {
+            const uint32_t t = __funnelshift_r(wp[0], wp[1], sh);
+            const float4 lo = lut[t & 15u], hi = lut[(t >> 4) & 15u];
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o8 + 8 * j), "f"(lo.x), "f"(lo.y),
+                         "f"(lo.z), "f"(lo.w), "f"(hi.x), "f"(hi.y), "f"(hi.z), "f"(hi.w) : "memory");
+        }
+    } else {
+        const int head = (int)((4 - (F0 & 3)) & 3);             // floats before the first aligned chunk
+        const int nchunk = (NF - head) >> 2;
+        const int tail0 = head + 4 * nchunk;
+        if (sl < head || (sl >= 4 && sl - 4 < NF - tail0)) {
+            const uint32_t fi = sl < 4 ? (uint32_t)sl : (uint32_t)(tail0 + sl - 4);
+            rec[fi] = (float)((W[fi >> 5] >> (fi & 31)) & 1u);
+        }
+        // chunk j = sl + L m starts at bit head + 4 sl + 4 L m: a lane-constant bit offset in
+        // word (head + 4 sl) / 32 + (L / 8) m
+        float4* o4 = reinterpret_cast<float4*>(rec + head);
+        const uint32_t q0 = (uint32_t)(head + 4 * sl), sh = q0 & 31u;
+        const uint32_t* wp = W + (q0 >> 5);
+        // (an ALU expansion of the 4 bits -- (t & 2^k) * (0x3F800000 >> k) -- instead of the LUT measured
+        // -0.2 % at 19x19 and -1 % at 9x9 in r02, although the L1 / shared pipe is the busiest unit)
 #pragma unroll 4
-    for (int j = sl; j < nchunk; j += L, wp += L / 8)
-        o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
+        for (int j = sl; j < nchunk; j += L, wp += L / 8)
+            o4[j] = lut[__funnelshift_r(wp[0], wp[1], sh) & 15u];
+    }
     g.sync();
 }
 
@@ -1045,7 +1072,10 @@ static int launch_observe(const uint16_t* pat, const uint8_t* role, float* obs, 
     const size_t smem = sizeof(BlockSmem<N>);
     cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t need = (n + boards_per_cta(N) - 1) / boards_per_cta(N);
-    int64_t grid = need < (int64_t)num_sms() * 4 ? need : (int64_t)num_sms() * 4;
+#ifndef BBK_GO_OBS_CTAS
+#define BBK_GO_OBS_CTAS 4
+#endif
+    int64_t grid = need < (int64_t)num_sms() * BBK_GO_OBS_CTAS ? need : (int64_t)num_sms() * BBK_GO_OBS_CTAS;
     observe_kernel<N><<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, smem, stream>>>(pat, role, obs, n);
     return (int)cudaGetLastError();
 }
