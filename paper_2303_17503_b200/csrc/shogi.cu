@@ -268,7 +268,31 @@ __device__ void build_and_emit_obs(WarpSmem& S, const float4* lut, const uint8_t
         }
         __syncwarp();
     }
-    if (obs_stream) {   // flat [n, 9, 9, 119] stream; records are not 16-B aligned
+#ifndef BBK_SHOGI_OBS_V8
+#define BBK_SHOGI_OBS_V8 1
+#endif
+    if (obs_stream && BBK_SHOGI_OBS_V8) {   // 32-byte stores over the 32-B aligned interior
+        const int64_t F0 = b * (int64_t)NF;
+        const int head = (int)((8 - (F0 & 7)) & 7);
+        const int nchunk = (NF - head) >> 3;
+        const int tail0 = head + 8 * nchunk;
+        float* rec = obs_stream + F0;
+        if (lane < head || (lane >= 8 && lane - 8 < NF - tail0)) {   // at most 7 edge floats each side
+            const uint32_t fi = lane < 8 ? (uint32_t)lane : (uint32_t)(tail0 + lane - 8);
+            rec[fi] = (float)((S.bits[fi >> 5] >> (fi & 31)) & 1u);
+        }
+        // chunk j = lane + 32 m starts at bit head + 8 lane + 256 m: lane-constant shift
+        float* o8 = rec + head;
+        const uint32_t q0 = (uint32_t)(head + 8 * lane), sh = q0 & 31u;
+        const uint32_t* wp = S.bits + (q0 >> 5);
+#pragma unroll 2
+        for (int j = lane; j < nchunk; j += 32, wp += 8) {
+            const uint32_t t = __funnelshift_r(wp[0], wp[1], sh);
+            const float4 lo = lut[t & 15u], hi = lut[(t >> 4) & 15u];
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o8 + 8 * j), "f"(lo.x), "f"(lo.y),
+                         "f"(lo.z), "f"(lo.w), "f"(hi.x), "f"(hi.y), "f"(hi.z), "f"(hi.w) : "memory");
+        }
+    } else if (obs_stream) {   // flat [n, 9, 9, 119] stream; records are not 16-B aligned
         const int64_t F0 = b * (int64_t)NF;
         const int head = (int)((4 - (F0 & 3)) & 3);
         const int nchunk = (NF - head) >> 2;
