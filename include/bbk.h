@@ -208,6 +208,13 @@ int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int6
 int bbk_abi_version(void);
 const char* bbk_build_info(void);
 
+/* Checked builds (-DBBK_CHECKS=1, tools/checked_build.sh): 1 if this library records failed
+ * scratch-index / capacity checks. bbk_debug_failures writes, per translation unit (go, chess,
+ * shogi, backgammon, small, mcts, fingerprint, util), (first failing source line << 32) | count,
+ * optionally clears them, and returns how many units recorded a failure (always 0 unchecked). */
+int bbk_debug_checks(void);
+int bbk_debug_failures(int reset, unsigned long long* out, int n);
+
 /* Batched rollouts (agents.py:113-116 over a batch): after each step, record every slot's first
  * finished episode -- returns [n, players] by player and its length -- into done / returns /
  * lengths, and add the number of newly finished slots to *count. */

@@ -92,6 +92,8 @@ def _declare(L):
 
     sig("bbk_abi_version", restype=C.c_int)
     sig("bbk_build_info", restype=C.c_char_p)
+    sig("bbk_debug_checks", restype=C.c_int)
+    sig("bbk_debug_failures", [C.c_int, P, C.c_int], C.c_int)
     sig("bbk_go_pat_stride", [C.c_int])
     sig("bbk_go_init", [C.c_int, ptr(Cols), ptr(GoState), ptr(GoStore), I64, I64, U64, P, I32, P])
     sig("bbk_go_step", [C.c_int, C.c_double, C.c_int, ptr(Cols), ptr(GoState), ptr(Cols), ptr(GoState), ptr(GoStore),

@@ -354,3 +354,6 @@ int bbk_bg_observe(const bbk_bg_state* s, const uint8_t* role, float* obs, int64
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_backgammon)

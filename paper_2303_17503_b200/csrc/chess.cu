@@ -199,6 +199,7 @@ __device__ void build_tasks(const uint8_t* bd, int side, uint16_t (*task)[96], i
     const int tot = __shfl_sync(BBK_FULL, incl, 31);
     n_own = tot & 0xFFFF; n_opp = tot >> 16;
     int ko = (incl - mine) & 0xFFFF, kx = (incl - mine) >> 16;
+    BBK_CHECK(n_own <= 96 && n_opp <= 96);   // task list capacity (WarpSmem::task)
     auto put = [&](uint16_t* list, int& k, int sq, uint8_t pc, int n) {
         const int t = pc & 7;
         if (n == 1) { list[k++] = (uint16_t)(sq | (8 << 6)); return; }
@@ -587,6 +588,7 @@ __global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 5
         const uint32_t meta_key = (uint32_t)side | ((uint32_t)castle << 8) | ((uint32_t)(uint8_t)ep_eff << 16);
         int reps = 0;
         const int window = halfmove < step ? halfmove : step;
+        BBK_CHECK(window < RING);   // the scanned plies are still in the ring (half-move clock <= 100)
         for (int j = lane; 2 * (j + 1) <= window; j += 32) {
             const int ply = step - 2 * (j + 1);
             const uint32_t m = S.pf_meta[ply & (RING - 1)];   // window <= half-move clock: prefetched
@@ -854,3 +856,6 @@ int bbk_chess_observe(const bbk_chess_state* s, const int32_t* step_count, const
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_chess)

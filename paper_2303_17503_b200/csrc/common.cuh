@@ -10,6 +10,39 @@
 
 #define BBK_FULL 0xffffffffu
 
+// Checked builds (-DBBK_CHECKS=1, tools/checked_build.sh): BBK_CHECK(cond) records the first failing
+// source line of each translation unit in a device word instead of trapping (a trap would poison the
+// context of the whole test run); bbk_debug_failures() (util.cu) collects and clears them. The pool's
+// compute-sanitizer is closed, so scratch-index / capacity asserts at every phase-multiplexed or
+// capacity-bounded buffer are the bad-access check. Off (no code) in the product build.
+#ifndef BBK_CHECKS
+#define BBK_CHECKS 0
+#endif
+#if BBK_CHECKS
+static __device__ unsigned long long g_bbk_fail;   // (line << 32) | count of failed checks, per TU
+#define BBK_CHECK(c)                                                                          \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            atomicCAS(&g_bbk_fail, 0ull, (unsigned long long)__LINE__ << 32);                 \
+            atomicAdd(&g_bbk_fail, 1ull);                                                     \
+        }                                                                                     \
+    } while (0)
+#define BBK_CHECK_READER(name)                                                                \
+    unsigned long long name(int reset) {                                                      \
+        unsigned long long v = 0ull;                                                          \
+        if (cudaMemcpyFromSymbol(&v, g_bbk_fail, sizeof v) != cudaSuccess) return ~0ull;      \
+        if (reset) {                                                                          \
+            const unsigned long long z = 0ull;                                                \
+            cudaMemcpyToSymbol(g_bbk_fail, &z, sizeof z);                                     \
+        }                                                                                     \
+        return v;                                                                             \
+    }
+#else
+#define BBK_CHECK(c) do { } while (0)
+#define BBK_CHECK_READER(name) \
+    unsigned long long name(int) { return 0ull; }
+#endif
+
 namespace bbk {
 
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {

@@ -317,3 +317,6 @@ int bbk_blake2b16_host(const uint8_t* msg, int64_t len, uint8_t* out) {
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_fingerprint)

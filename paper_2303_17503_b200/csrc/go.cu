@@ -313,14 +313,18 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         int k = off;
         for (uint32_t s_ = SX; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
+            BBK_CHECK(k < WarpSmem<N>::MAXR && r < N);
             U.run[k] = (uint16_t)((0u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(X >> s)) - 1));
             const uint16_t l = lab[r * N + s];
+            BBK_CHECK(l < N * N);
             U.root[k] = l;
         }
         for (uint32_t s_ = SY; s_; s_ &= s_ - 1, k++) {
             int s = __ffs(s_) - 1;
+            BBK_CHECK(k < WarpSmem<N>::MAXR && r < N);
             U.run[k] = (uint16_t)((1u << 15) | ((uint32_t)r << 10) | ((uint32_t)s << 5) | (uint32_t)(__ffs(~(Y >> s)) - 1));
             const uint16_t l = lab[r * N + s];
+            BBK_CHECK(l < N * N);
             U.root[k] = l;
         }
     }
@@ -336,6 +340,8 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         const uint32_t up = rr > 0 ? run & S.rE[rr - 1] : 0u, dn = rr < N - 1 ? run & S.rE[rr + 1] : 0u;
         const uint32_t sd = ((run << 1) | (run >> 1)) & S.rE[rr];
         if (!(up | dn | sd)) continue;
+        // a label is a stone of its chain: its stats word never shares a point with a capture XOR
+        BBK_CHECK(x < N * N && !((S.rE[x / N] >> (x % N)) & 1u));
         const uint32_t lo = up ? (rr - 1) * N + __ffs(up) - 1 : sd ? rr * N + __ffs(sd) - 1 : (rr + 1) * N + __ffs(dn) - 1;
         const uint32_t hi = dn ? (rr + 1) * N + 31 - __clz(dn) : sd ? rr * N + 31 - __clz(sd) : (rr - 1) * N + 31 - __clz(up);
         atomicOr(&gst[2 * x], 0x80000000u | (lo | hi) | (((~lo | ~hi) & 0x3FFu) << 10));
@@ -359,6 +365,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         const uint32_t e = U.run[i];
         if ((e >> 15) && at && (gs & 0x80000000u)) {
             const uint32_t lib = gs & 0x3FFu;
+            BBK_CHECK(lib < N * N && ((S.rE[lib / N] >> (lib % N)) & 1u));   // a capture point is empty
             atomicOr(&S.rcap[lib / N], 1u << (lib % N));
             const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
             const uint64_t x = zrun<N>(rr, s, len, ycol);
@@ -404,6 +411,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
                 const uint32_t gs = gst[2 * U.root[i]];
                 if ((gs & (gs >> 10) & 0x3FFu) != 0u) continue;   // >= 2 liberties
                 const uint32_t lib = gs & 0x3FFu;
+                BBK_CHECK(lib < N * N);
                 if (!((S.rcap[lib / N] >> (lib % N)) & 1u)) continue;
                 const int rr = (e >> 10) & 31, s = (e >> 5) & 31, len = e & 31;
                 const uint64_t x = zrun<N>(rr, s, len, 1 - ycol);
@@ -448,6 +456,7 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         }
         g.sync();
         unsigned found = 0u;
+        BBK_CHECK(nscan >= 0 && nscan <= (int)0x7FFFFFFF);
         for (int j = r; j < nscan + 1; j += L) {
             uint64_t v = j < nscan ? hist[j] : extra;
             for (unsigned a_ = active; a_; a_ &= a_ - 1) {
@@ -493,6 +502,7 @@ __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, flo
     constexpr int NW = (NF + 31) / 32;
     for (int w = sl; w < NW; w += L) {
         const uint32_t q = 32u * w, c = (q * 61681u) >> 20, k = q - 17u * c;   // q / 17, exact for q < 65536
+        BBK_CHECK(c == q / 17u && c + 2 < (uint32_t)pat_stride(N));
         uint32_t v = (P[c] >> k) | (P[c + 1] << (17 - k));
         if (k > 2) v |= P[c + 2] << (34 - k);
         W[w] = v;
@@ -519,6 +529,7 @@ __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, flo
         float* o8 = rec + head;
         const uint32_t q0 = (uint32_t)(head + 8 * sl), sh = q0 & 31u;
         const uint32_t* wp = W + (q0 >> 5);
+        BBK_CHECK(nchunk <= 0 || (head + 8 * (nchunk - 1)) / 32 + 1 <= NW);   // last chunk's words are staged
 #pragma unroll 2
         for (int j = sl; j < nchunk; j += L, wp += L / 4) {
             const uint32_t t = __funnelshift_r(wp[0], wp[1], sh);
@@ -780,6 +791,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                     const uint32_t Mu = g.shfl(M, ra > 0 ? ra - 1 : 0);
                     const uint32_t Md = g.shfl(M, ra < N - 1 ? ra + 1 : 0);
                     constexpr uint32_t NONE = 0xFFFFu;   // never a label (labels < C)
+                    BBK_CHECK(a >= 0 && a < C && ra < N && ca < N);
                     const uint32_t lu = (ra > 0 && ((Mu >> ca) & 1u)) ? lab[a - N] : NONE;
                     const uint32_t ld = (ra < N - 1 && ((Md >> ca) & 1u)) ? lab[a + N] : NONE;
                     const uint32_t ll = (ca > 0 && ((Mr >> (ca - 1)) & 1u)) ? lab[a - 1] : NONE;
@@ -843,6 +855,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 if (role == 0) { Bk = M; Wh = O; } else { Wh = M; Bk = O; }
                 counts = g.sum(__popc(Bk) | (__popc(Wh) << 16));
                 const int nbk = counts & 0xFFFF, nwh = counts >> 16;
+                BBK_CHECK(hlen < p.store.hist_cap);   // the superko history's capacity
                 if (sl == 0) {
                     hist[hlen] = h2;
                     bloom_add<N>(gbloom, h2);
@@ -893,6 +906,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         // stage mask bytes at the destination's 16-byte phase and emit
         const int64_t mstart = b * (int64_t)A;
         const int moff = (int)(mstart & 15);
+        BBK_CHECK(moff + C < (int)sizeof(S.u.mb));
         if (sl < N) {
             for (int col = 0; col < N; col++) S.u.mb[moff + sl * N + col] = (uint8_t)((legal >> col) & 1u);
         }
@@ -1164,3 +1178,6 @@ int bbk_go_rebuild_bloom(int size, const bbk_go_store* store, const int32_t* his
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_go)

@@ -408,3 +408,6 @@ int bbk_mt19937_host(uint64_t seed, const uint32_t* below, int64_t n, uint32_t* 
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_mcts)

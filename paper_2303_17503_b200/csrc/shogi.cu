@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                 if (lane >= o) incl += t;
             }
             const int ntask = __shfl_sync(BBK_FULL, incl, 31);
+            BBK_CHECK(ntask <= 320);   // task list capacity (WarpSmem::task)
             int k = incl - mine;
 #pragma unroll
             for (int j = 0; j < 3; j++)
@@ -682,6 +683,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
             cur = nxt;
             pf_ready = true;
         }
+        BBK_CHECK(step < cap - BLOOM_U64);   // the key log ends where its Bloom filter starts
         if (lane == 0) {
             hist[step] = key;
             atomicOr(&bloom[i1 >> 5], 1u << (i1 & 31));
@@ -823,3 +825,6 @@ int bbk_shogi_observe(const bbk_shogi_state* s, const int32_t* step_count, const
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_shogi)

@@ -204,3 +204,6 @@ int bbk_small_observe(int game, const uint8_t* blob, const uint8_t* terminated, 
 }
 
 }  // extern "C"
+
+// checked builds: this translation unit's failed-check word (common.cuh BBK_CHECK)
+BBK_CHECK_READER(bbk_tu_fail_small)

@@ -129,6 +129,11 @@ __global__ void latch_finished_kernel(const uint8_t* term, const uint8_t* trunc,
 
 }  // namespace util
 
+// per-translation-unit failed-check readers (common.cuh BBK_CHECK_READER)
+unsigned long long bbk_tu_fail_go(int), bbk_tu_fail_chess(int), bbk_tu_fail_shogi(int), bbk_tu_fail_backgammon(int),
+    bbk_tu_fail_small(int), bbk_tu_fail_mcts(int), bbk_tu_fail_fingerprint(int);
+BBK_CHECK_READER(bbk_tu_fail_util)
+
 extern "C" {
 
 int bbk_random_actions(const uint8_t* mask, int64_t n, int32_t num_actions, uint64_t key_state,
@@ -170,7 +175,22 @@ int bbk_latch_finished(const uint8_t* term, const uint8_t* trunc, const float* r
 int bbk_abi_version(void) { return BBK_ABI_VERSION; }
 
 const char* bbk_build_info(void) {
-    return "libbbk: sm_100a (compute_100a)";
+    return BBK_CHECKS ? "libbbk: sm_100a (compute_100a), checked build (BBK_CHECKS)" : "libbbk: sm_100a (compute_100a)";
+}
+
+int bbk_debug_checks(void) { return BBK_CHECKS; }
+
+int bbk_debug_failures(int reset, unsigned long long* out, int n) {
+    unsigned long long (*const tus[])(int) = {bbk_tu_fail_go, bbk_tu_fail_chess, bbk_tu_fail_shogi,
+                                              bbk_tu_fail_backgammon, bbk_tu_fail_small, bbk_tu_fail_mcts,
+                                              bbk_tu_fail_fingerprint, bbk_tu_fail_util};
+    int bad = 0;
+    for (int i = 0; i < 8; i++) {
+        const unsigned long long v = tus[i](reset);
+        if (i < n && out) out[i] = v;
+        bad += v != 0ull;
+    }
+    return bad;
 }
 
 }  // extern "C"

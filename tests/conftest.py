@@ -68,3 +68,34 @@ def reference_optional():
     import boardbatch
 
     return boardbatch
+
+
+_TUS = ("go", "chess", "shogi", "backgammon", "small", "mcts", "fingerprint", "util")
+
+
+@pytest.fixture(autouse=True)
+def _checked_build(request):
+    """BBK_EXPECT_CHECKED=1 (with BBK_LIB pointing at tools/checked_build.sh's library): every GPU test
+    must leave the device-side scratch-index / capacity checks clean (common.cuh BBK_CHECK)."""
+    if os.environ.get("BBK_EXPECT_CHECKED") != "1" or "gpu" not in request.keywords:
+        yield
+        return
+    import ctypes
+
+    from paper_2303_17503_b200 import _native
+
+    L = _native.lib()
+    assert L.bbk_debug_checks() == 1, "BBK_EXPECT_CHECKED=1 but the loaded library is not a checked build"
+    out = (ctypes.c_ulonglong * len(_TUS))()
+    L.bbk_debug_failures(1, out, len(_TUS))   # clear
+    yield
+    import torch
+
+    torch.cuda.synchronize()
+    bad = L.bbk_debug_failures(1, out, len(_TUS))
+    fails = {t: (v >> 32, v & 0xFFFFFFFF) for t, v in zip(_TUS, out) if v}
+    log = os.environ.get("BBK_CHECK_LOG")
+    if log:
+        with open(log, "a") as fh:
+            fh.write(f"{request.node.nodeid} {'FAIL ' + repr(fails) if bad else 'clean'}\n")
+    assert not bad, f"device checks failed (unit: (first line, count)): {fails}"

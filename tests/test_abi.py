@@ -32,6 +32,9 @@ def test_library_exports_every_declared_symbol():
     for n in (5, 7, 9, 11, 13, 15, 17, 19):   # host allocation == kernel row stride
         assert L.bbk_go_filter_words(n) == GoKernel(n).filter_words
     assert L.bbk_go_filter_words(8) == -1
+    # the product build carries no device-side checks (tools/checked_build.sh makes the checked one)
+    if not os.environ.get("BBK_LIB"):
+        assert L.bbk_debug_checks() == 0
 
 
 def test_library_is_sm100a():
