@@ -442,7 +442,9 @@ def run_e2e(args, game, dev, world, slot0, B):
             h["cp"].copy_(d.current_player, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
-        main.synchronize()        # the next actions are in host memory
+        # no host wait for the step itself: the next step's kernel reads the next actions from the
+        # pinned buffer in stream order, so the host runs at most one step ahead of the GPU (it
+        # waits for the previous step's results right here)
         if pending:
             read(pending.pop())
         pending.append((batch, ev, h))
