@@ -336,13 +336,15 @@ def run_gpu(args, rank, world, local):
 
 
 def go19_windows(args, dev, slot0, B):
-    """Two windows beside the driver's (early-game) K: the full episode cycle (slots truncate in
-    phase at max_steps = 512, so 512 steps after a 16-step warm-up cover every phase once), and a
-    late-game window (steps 401..432: long superko histories, crowded boards)."""
+    """Windows beside the driver's (early-game) K: the full episode cycle (slots truncate in
+    phase at max_steps = 512, so 512 steps after a 16-step warm-up cover every phase once), a
+    late-game window (steps 401..432: long superko histories, crowded boards), and SURVEY §8(d)
+    config 2's steady-state window (1024 steps after a 512-step warm-up: two cycles, every slot
+    past its first reset)."""
     import torch
 
     res = {}
-    for name, W, K in (("full_cycle", 16, 512), ("late_game", 400, 32)):
+    for name, W, K in (("full_cycle", 16, 512), ("late_game", 400, 32), ("survey_config2", 512, 1024)):
         loop = DeviceLoop("go_19x19", B, slot0, dev, args.seed)
         for _ in range(W):
             loop.step()
@@ -380,6 +382,16 @@ def game_block(args, game, dev):
             out["reference_cpu"] = reference_python(game, args.seed, min(args.cpu_seconds, 6.0))
     if game == "go_9x9":
         out["baseline_config1"] = baseline_config1(args)
+    if game == "backgammon":   # SURVEY §8(d) config 5's window: 2048 steps after a 1024-step warm-up
+        loop = DeviceLoop(game, B, 0, dev, args.seed)
+        for _ in range(1024):
+            loop.step()
+        torch.cuda.synchronize()
+        ms, kern_ms = loop.timed(2048)
+        del loop
+        out["survey_config5_window"] = {"value": B * 2048 / (ms / 1e3), "steps": 2048, "warmup": 1024,
+                                        "ms_per_step": ms / 2048,
+                                        "roofline_frac": roofline(game, B, kern_ms, ms / 2048)["frac"]}
     return out
 
 
