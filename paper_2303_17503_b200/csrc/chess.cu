@@ -803,12 +803,15 @@ __global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, co
     obs[idx] = val;
 }
 
+#ifndef BBK_CHESS_GRID_BOARDS
+#define BBK_CHESS_GRID_BOARDS 4   // boards per warp per launch (common.cuh step_grid); 0: persistent grid (r02: 4 = +6 %, 3 = +6.1 %, 8 = +3 %)
+#endif
 static int launch(const Params& p, cudaStream_t s) {
     const int64_t need = (p.n + kWarps - 1) / kWarps;
     if (p.load_board) {
-        step_kernel<true><<<(unsigned)persistent_grid(step_kernel<true>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+        step_kernel<true><<<(unsigned)step_grid(step_kernel<true>, kWarps * 32, 0, need, BBK_CHESS_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
     } else {
-        step_kernel<false><<<(unsigned)persistent_grid(step_kernel<false>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+        step_kernel<false><<<(unsigned)step_grid(step_kernel<false>, kWarps * 32, 0, need, BBK_CHESS_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
     }
     return (int)cudaGetLastError();
 }

@@ -87,6 +87,16 @@ inline int64_t persistent_grid(Kernel kernel, int threads, size_t smem, int64_t 
     return grid < 1 ? 1 : grid;
 }
 
+// boards_per_warp > 0: a non-persistent grid of `need / boards_per_warp` CTAs (each warp handles a
+// few boards, CTAs retire and start in board order -- a tighter write window for the observation
+// stream, see go.cu launch_step); 0: the persistent grid above.
+template <class Kernel>
+inline int64_t step_grid(Kernel kernel, int threads, size_t smem, int64_t need, int boards_per_warp) {
+    if (boards_per_warp <= 0) return persistent_grid(kernel, threads, smem, need);
+    const int64_t g = (need + boards_per_warp - 1) / boards_per_warp;
+    return g < 1 ? 1 : g;
+}
+
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
     uint32_t lo = __shfl_sync(BBK_FULL, (uint32_t)v, src);
     uint32_t hi = __shfl_sync(BBK_FULL, (uint32_t)(v >> 32), src);

@@ -646,6 +646,9 @@ __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
 constexpr int kNbUnroll = BBK_GO_NB_UNROLL;
 
 // resident CTAs per SM the register budget is sized for: small boards fit 8 (shared memory allows it)
+#ifndef BBK_GO_GRID_BOARDS
+#define BBK_GO_GRID_BOARDS -1   // boards per warp segment per launch: 0 persistent, -1 per-size default
+#endif
 #ifndef BBK_GO_CTAS_SMALL
 #define BBK_GO_CTAS_SMALL 8
 #endif
@@ -1074,7 +1077,15 @@ static int launch_step(const StepParams& p, cudaStream_t stream) {
     }
     const int per_sm = per_sm_dev[dev];
     int64_t need = (p.n + boards_per_cta(N) - 1) / boards_per_cta(N);
+    // Grid: boards up to 13x13 use a persistent grid (the resident CTAs loop over all boards); the
+    // large boards launch one CTA per 4 boards per warp segment, so CTAs retire and new ones start in
+    // board order. The observation stream then leaves the SMs in a tighter address window: a warp
+    // writing whole records absorbs 7.2 TB/s when each warp writes one record and exits vs 6.2 TB/s
+    // from a persistent grid (tools/write_pattern.cu); go_19x19 +11.5 % early game, +4 % over a full
+    // episode cycle, +1 % late game (r02 A/B, 2-6 boards per warp within 1 %). 9x9 lost 3.7 %.
+    constexpr int kGridBoards = BBK_GO_GRID_BOARDS >= 0 ? BBK_GO_GRID_BOARDS : (N > 13 ? 4 : 0);
     int64_t grid = (int64_t)num_sms() * per_sm;
+    if (kGridBoards > 0) grid = (need + kGridBoards - 1) / kGridBoards;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
     step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(p);
@@ -1085,11 +1096,10 @@ template <int N>
 static int launch_observe(const uint16_t* pat, const uint8_t* role, float* obs, int64_t n, cudaStream_t stream) {
     const size_t smem = sizeof(BlockSmem<N>);
     cudaFuncSetAttribute(observe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int64_t need = (n + boards_per_cta(N) - 1) / boards_per_cta(N);
-#ifndef BBK_GO_OBS_CTAS
-#define BBK_GO_OBS_CTAS 4
-#endif
-    int64_t grid = need < (int64_t)num_sms() * BBK_GO_OBS_CTAS ? need : (int64_t)num_sms() * BBK_GO_OBS_CTAS;
+    // one board per warp segment, CTAs retire in board order (a pure observation stream: 7.2 vs
+    // 6.2 TB/s from a persistent grid, tools/write_pattern.cu)
+    const int64_t need = (n + boards_per_cta(N) - 1) / boards_per_cta(N);
+    const int64_t grid = need;
     observe_kernel<N><<<(unsigned)(grid < 1 ? 1 : grid), kWarps * 32, smem, stream>>>(pat, role, obs, n);
     return (int)cudaGetLastError();
 }

@@ -770,12 +770,15 @@ __global__ void __launch_bounds__(kWarps * 32) observe_kernel(bbk_shogi_state st
     }
 }
 
+#ifndef BBK_SHOGI_GRID_BOARDS
+#define BBK_SHOGI_GRID_BOARDS 1   // boards per warp per launch (common.cuh step_grid); 0: persistent grid (r02: 1 = +2.3 %, 2 = +0.5 %, 4 = -2.6 %)
+#endif
 static int launch(const Params& p, cudaStream_t s) {
     const int64_t need = (p.n + kWarps - 1) / kWarps;
     if (p.load_board) {
-        step_kernel<true><<<(unsigned)persistent_grid(step_kernel<true>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+        step_kernel<true><<<(unsigned)step_grid(step_kernel<true>, kWarps * 32, 0, need, BBK_SHOGI_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
     } else {
-        step_kernel<false><<<(unsigned)persistent_grid(step_kernel<false>, kWarps * 32, 0, need), kWarps * 32, 0, s>>>(p);
+        step_kernel<false><<<(unsigned)step_grid(step_kernel<false>, kWarps * 32, 0, need, BBK_SHOGI_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
     }
     return (int)cudaGetLastError();
 }

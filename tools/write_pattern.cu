@@ -56,6 +56,40 @@ __global__ void flat_unroll4(float4* out, int64_t n4) {
         for (int u = 0; u < 4; u++) out[i + u * stride] = make_float4(1.f, 1.f, 1.f, 1.f);
     }
 }
+__device__ __forceinline__ void st256cs(float* p, float v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st256na(float* p, float v) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st256ef(float* p, float v) {
+    asm volatile("st.global.L2::evict_first.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "f"(v) : "memory");
+}
+template <int MODE>
+__global__ void per_record256m(float* out, int64_t n, int rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < n; b += nw) {
+        const int64_t F0 = b * rec;
+        const int head = (int)((8 - (F0 & 7)) & 7);
+        const int nchunk = (rec - head) >> 3;
+        float* o = out + F0 + head;
+        const float v = (float)(b & 1);
+        for (int j = lane; j < nchunk; j += 32) {
+            if (MODE == 0) st256cs(o + 8 * j, v);
+            else if (MODE == 1) st256na(o + 8 * j, v);
+            else st256ef(o + 8 * j, v);
+        }
+    }
+}
+template <int MODE>
+__global__ void flat256m(float* out, int64_t n8) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+        if (MODE == 0) st256cs(out + 8 * i, 1.0f);
+        else if (MODE == 1) st256na(out + 8 * i, 1.0f);
+        else st256ef(out + 8 * i, 1.0f);
+    }
+}
 // per-record with 32-byte stores over the 32-B aligned interior
 __global__ void per_record256(float* out, int64_t n, int rec) {
     const int lane = threadIdx.x & 31;
@@ -67,6 +101,55 @@ __global__ void per_record256(float* out, int64_t n, int rec) {
         float* o = out + F0 + head;
         const float v = (float)(b & 1);
         for (int j = lane; j < nchunk; j += 32) st256(o + 8 * j, v);
+    }
+}
+
+__device__ __forceinline__ void write_rec256(float* out, int64_t b, int rec, int lane) {
+    const int64_t F0 = b * rec;
+    const int head = (int)((8 - (F0 & 7)) & 7);
+    const int nchunk = (rec - head) >> 3;
+    float* o = out + F0 + head;
+    const float v = (float)(b & 1);
+    for (int j = lane; j < nchunk; j += 32) st256(o + 8 * j, v);
+}
+// (a) persistent, boards taken from a global counter in order (dynamic scheduling)
+__global__ void rec_dynamic(float* out, int64_t n, int rec, unsigned long long* ctr) {
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(ctr, 1ull);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if ((int64_t)b >= n) break;
+        write_rec256(out, (int64_t)b, rec, lane);
+    }
+}
+// (b) persistent, each warp a contiguous range of boards
+__global__ void rec_ranges(float* out, int64_t n, int rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int64_t per = (n + nw - 1) / nw;
+    for (int64_t b = w * per; b < n && b < (w + 1) * per; b++) write_rec256(out, b, rec, lane);
+}
+// (c) non-persistent, K consecutive boards per warp
+template <int K>
+__global__ void rec_nonpersist_k(float* out, int64_t n, int rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    for (int k = 0; k < K; k++) {
+        const int64_t b = w * K + k;
+        if (b < n) write_rec256(out, b, rec, lane);
+    }
+}
+// (d) non-persistent, K boards per warp strided by the number of warps in the grid (interleaved)
+template <int K>
+__global__ void rec_nonpersist_strided(float* out, int64_t n, int rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    for (int k = 0; k < K; k++) {
+        const int64_t b = w + k * nw;
+        if (b < n) write_rec256(out, b, rec, lane);
     }
 }
 
@@ -98,6 +181,29 @@ int main() {
         char nm[64];
         snprintf(nm, sizeof nm, "warp per record 256-bit, %d x 4 / SM", ctas);
         timeit(nm, [&] { per_record256<<<148 * ctas, 128>>>(out, n, rec); });
+    }
+    unsigned long long* ctr;
+    cudaMalloc(&ctr, 8);
+    timeit("per record 256, persistent dynamic counter 6x4", [&] { cudaMemsetAsync(ctr, 0, 8); rec_dynamic<<<148 * 6, 128>>>(out, n, rec, ctr); });
+    timeit("per record 256, persistent contiguous ranges 6x4", [&] { rec_ranges<<<148 * 6, 128>>>(out, n, rec); });
+    timeit("per record 256, non-persistent 4 consecutive/warp", [&] { rec_nonpersist_k<4><<<(unsigned)(n / 16), 128>>>(out, n, rec); });
+    timeit("per record 256, non-persistent 16 consecutive/warp", [&] { rec_nonpersist_k<16><<<(unsigned)(n / 64), 128>>>(out, n, rec); });
+    timeit("per record 256, non-persistent 4 strided/warp", [&] { rec_nonpersist_strided<4><<<(unsigned)(n / 16), 128>>>(out, n, rec); });
+    timeit("per record 256, NON-persistent (n/4 CTAs)", [&] { per_record256<<<(unsigned)(n / 4), 128>>>(out, n, rec); });
+    timeit("per record 128, NON-persistent (n/4 CTAs)", [&] { per_record<<<(unsigned)(n / 4), 128>>>(out, n, rec, 0); });
+    timeit("flat 256, NON-persistent (1 chunk/thread)", [&] { flat256<<<(unsigned)(bytes / 32 / 256), 256>>>(out, (int64_t)(bytes / 32)); });
+    timeit("flat 128, NON-persistent (1 chunk/thread)", [&] { flat<<<(unsigned)(bytes / 16 / 256), 256>>>((float4*)out, (int64_t)(bytes / 16)); });
+    timeit("flat 256 .cs", [&] { flat256m<0><<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
+    timeit("flat 256 L1::no_allocate", [&] { flat256m<1><<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
+    timeit("flat 256 L2::evict_first", [&] { flat256m<2><<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
+    timeit("per record 256 .cs, 6x4", [&] { per_record256m<0><<<148 * 6, 128>>>(out, n, rec); });
+    timeit("per record 256 no_allocate, 6x4", [&] { per_record256m<1><<<148 * 6, 128>>>(out, n, rec); });
+    timeit("per record 256 evict_first, 6x4", [&] { per_record256m<2><<<148 * 6, 128>>>(out, n, rec); });
+    timeit("flat 256 (again)", [&] { flat256<<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
+    for (int t : {128, 512, 1024}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "flat 256, %d threads x 148x(2048/%d)", t, t);
+        timeit(nm, [&] { flat256<<<148 * (2048 / t), t>>>(out, (int64_t)(bytes / 32)); });
     }
     for (int ctas : {4, 6, 8, 16}) {
         char nm[64];
