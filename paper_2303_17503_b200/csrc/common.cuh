@@ -87,14 +87,26 @@ inline int64_t persistent_grid(Kernel kernel, int threads, size_t smem, int64_t 
     return grid < 1 ? 1 : grid;
 }
 
-// boards_per_warp > 0: a non-persistent grid of `need / boards_per_warp` CTAs (each warp handles a
-// few boards, CTAs retire and start in board order -- a tighter write window for the observation
-// stream, see go.cu launch_step); 0: the persistent grid above.
+// Grid of a step launch. boards_per_warp <= 0: the persistent grid above. Otherwise whole waves
+// of resident CTAs (about need / boards_per_warp CTAs, rounded to a multiple of the resident
+// count so the last wave is not a partial one): CTAs retire and start in board order, which gives
+// the observation stream a tighter write window (go.cu launch_step); a batch that does not fill
+// the resident CTAs keeps one board per warp.
+inline int64_t wave_grid(int64_t resident, int64_t need, int boards_per_warp) {
+    if (resident < 1) resident = 1;
+    if (boards_per_warp <= 0 || need <= resident) return need < resident ? (need < 1 ? 1 : need) : resident;
+    int64_t waves = (need + resident * boards_per_warp / 2) / (resident * boards_per_warp);
+    if (waves < 1) waves = 1;
+    const int64_t g = resident * waves;
+    return g < need ? g : need;
+}
 template <class Kernel>
 inline int64_t step_grid(Kernel kernel, int threads, size_t smem, int64_t need, int boards_per_warp) {
-    if (boards_per_warp <= 0) return persistent_grid(kernel, threads, smem, need);
-    const int64_t g = (need + boards_per_warp - 1) / boards_per_warp;
-    return g < 1 ? 1 : g;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    return wave_grid((int64_t)sms * (per_sm < 1 ? 1 : per_sm), need, boards_per_warp);
 }
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {

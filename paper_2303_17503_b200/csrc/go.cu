@@ -1084,10 +1084,7 @@ static int launch_step(const StepParams& p, cudaStream_t stream) {
     // from a persistent grid (tools/write_pattern.cu); go_19x19 +11.5 % early game, +4 % over a full
     // episode cycle, +1 % late game (r02 A/B, 2-6 boards per warp within 1 %). 9x9 lost 3.7 %.
     constexpr int kGridBoards = BBK_GO_GRID_BOARDS >= 0 ? BBK_GO_GRID_BOARDS : (N > 13 ? 4 : 0);
-    int64_t grid = (int64_t)num_sms() * per_sm;
-    if (kGridBoards > 0) grid = (need + kGridBoards - 1) / kGridBoards;
-    if (grid > need) grid = need;
-    if (grid < 1) grid = 1;
+    const int64_t grid = wave_grid((int64_t)num_sms() * per_sm, need, kGridBoards);
     step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(p);
     return (int)cudaGetLastError();
 }

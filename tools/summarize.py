@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 MARK = "<!-- history -->"
-GAMES = [("go19", "go_19x19", "go_19x19 (K=512, full episode cycle)", 131072, "-s 250"),
+GAMES = [("go19", "go_19x19", "go_19x19 (default window)", 131072, "-s 250"),
          ("chess", "chess", "chess", 131072, "-s 100"),
          ("shogi", "shogi", "shogi (B=2^16)", 65536, "-s 100"),
          ("backgammon", "backgammon", "backgammon", 131072, "-s 100"),
@@ -54,6 +54,9 @@ def main():
                     f"{d['e2e']['value'] / 1e6:.1f} M | {v['dram_bytes_per_env_step']:,.0f} | {v['b_alg']:,} | "
                     f"{v['issue_active_pct']:.0f} % | {v['warp_inst_per_env_step']:,.0f} |")
     go = line(os.path.join(dst, "bench_go19.json"))
+    for name, w in go.get("windows", {}).items():
+        rows.insert(1, f"| go_19x19 window `{name}` (W={w['warmup']}, K={w['steps']}) | {w['value'] / 1e6:.1f} M | "
+                       f"{w['ms_per_step']:.3f} | {w['roofline_frac']:.3f} | | | | | |")
     ref = line(os.path.join(dst, "bench_reference.json"))
     sweeps = []
     for short, key, *_ in GAMES[:3]:
@@ -62,8 +65,8 @@ def main():
                                                  for e in range(10, 18)) + " |")
     head = f"""# {rnd} measurement pass (tools/gpu_measure.sh on one B200; tools/summarize.py)
 
-`python bench.py` defaults: B = 2^17 per GPU (shogi 2^16), W = 16 (8 for the per-game lines), K = 512
-(256 per game), fused step kernel (one launch per step incl. next-step random actions and the episode
+`python bench.py` defaults: B = 2^17 per GPU (shogi 2^16), W = 8, K = 128 (the per-game lines of
+tools/gpu_measure.sh: K = 256), fused step kernel (one launch per step incl. next-step random actions and the episode
 counter), SM clock {go['clocks']['sm_mhz']:.0f} MHz (max {go['clocks']['sm_max_mhz']:.0f}), throttle reasons {go['clocks']['reasons']}.
 Roofline = B_alg x B / step-kernel CUDA-event time vs the measured {go['roofline']['peak']} GB/s copy peak
 (MEASURED_PEAKS.json).
