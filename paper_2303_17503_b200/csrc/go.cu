@@ -225,13 +225,25 @@ __device__ __forceinline__ uint32_t run_at(uint32_t X, int s) {
     return ((1u << len) - 1u) << s;
 }
 
+// Bloom probes per hash (13-bit slices of the 64-bit zobrist hash). A false positive costs an exact
+// scan of the env's history (up to 4 KB late in a 19x19 game): 4 probes halve the false-positive
+// rate of 3 at these fill levels (8192 bits, ~500 entries: 0.47 % -> 0.22 %).
+#ifndef BBK_GO_BLOOM_K
+#define BBK_GO_BLOOM_K 4
+#endif
+constexpr int kBloomK = BBK_GO_BLOOM_K;
+__device__ __forceinline__ uint32_t bloom_idx(uint64_t h, int j, uint32_t M) { return (uint32_t)(h >> (13 * j)) & M; }
+
 template <int N>
 __device__ __forceinline__ bool bloom_maybe(const uint32_t* bloom, uint64_t h) {
     constexpr uint32_t M = 32u * bloom_words(N) - 1u;
-    uint32_t i1 = (uint32_t)h & M;
-    uint32_t i2 = (uint32_t)(h >> 13) & M;
-    uint32_t i3 = (uint32_t)(h >> 26) & M;
-    return ((bloom[i1 >> 5] >> (i1 & 31)) & (bloom[i2 >> 5] >> (i2 & 31)) & (bloom[i3 >> 5] >> (i3 & 31)) & 1u) != 0;
+    uint32_t all = 1u;
+#pragma unroll
+    for (int j = 0; j < kBloomK; j++) {
+        const uint32_t i = bloom_idx(h, j, M);
+        all &= bloom[i >> 5] >> (i & 31);
+    }
+    return (all & 1u) != 0;
 }
 
 // Stone-count pair filter: a position can only repeat a history position with the same
@@ -250,9 +262,11 @@ __device__ __forceinline__ void pair_add(uint32_t* gb, int nb, int nw) {   // on
 template <int N>
 __device__ __forceinline__ void bloom_add(uint32_t* gb, uint64_t h) {
     constexpr uint32_t M = 32u * bloom_words(N) - 1u;
-    const uint32_t idx[3] = {(uint32_t)h & M, (uint32_t)(h >> 13) & M, (uint32_t)(h >> 26) & M};
 #pragma unroll
-    for (int j = 0; j < 3; j++) atomicOr(&gb[idx[j] >> 5], 1u << (idx[j] & 31));   // RED: no round trip
+    for (int j = 0; j < kBloomK; j++) {
+        const uint32_t i = bloom_idx(h, j, M);
+        atomicOr(&gb[i >> 5], 1u << (i & 31));   // RED: no round trip
+    }
 }
 
 template <int N, int L>
@@ -457,11 +471,21 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
         g.sync();
         unsigned found = 0u;
         BBK_CHECK(nscan >= 0 && nscan <= (int)0x7FFFFFFF);
-        for (int j = r; j < nscan + 1; j += L) {
-            uint64_t v = j < nscan ? hist[j] : extra;
-            for (unsigned a_ = active; a_; a_ &= a_ - 1) {
-                int l = __ffs(a_) - 1;
-                if (v == S.u.sk.hit[l]) found |= 1u << l;
+        // 4 history entries per lane in flight per iteration (the scan is latency-bound)
+        for (int j0 = r; j0 < nscan + 1; j0 += 4 * L) {
+            uint64_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * L;
+                v[u] = j < nscan ? hist[j] : j == nscan ? extra : ~extra;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (j0 + u * L > nscan) break;
+                for (unsigned a_ = active; a_; a_ &= a_ - 1) {
+                    int l = __ffs(a_) - 1;
+                    if (v[u] == S.u.sk.hit[l]) found |= 1u << l;
+                }
             }
         }
         found = g.reduce_or(found);
@@ -1016,10 +1040,11 @@ __global__ void rebuild_bloom_kernel(bbk_go_store st, const int32_t* hist_len, i
         const uint64_t* hist = st.history + b * (int64_t)st.hist_cap;
         for (int j = lane; j < hist_len[b]; j += 32) {
             uint64_t h = hist[j];
-            uint32_t i1 = (uint32_t)h & M, i2 = (uint32_t)(h >> 13) & M, i3 = (uint32_t)(h >> 26) & M;
-            atomicOr(&sb[w][i1 >> 5], 1u << (i1 & 31));
-            atomicOr(&sb[w][i2 >> 5], 1u << (i2 & 31));
-            atomicOr(&sb[w][i3 >> 5], 1u << (i3 & 31));
+#pragma unroll
+            for (int q = 0; q < kBloomK; q++) {
+                const uint32_t i = bloom_idx(h, q, M);
+                atomicOr(&sb[w][i >> 5], 1u << (i & 31));
+            }
         }
         __syncwarp();
         for (int i = lane; i < BW; i += 32) st.bloom[b * FW + i] = sb[w][i];
