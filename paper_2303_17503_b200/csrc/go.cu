@@ -47,7 +47,10 @@ __host__ __device__ constexpr int boards_per_cta(int N) { return kWarps * (32 / 
 // traffic (1,280 B at 19x19 against a 25.9 KB step, but 21 % of a 9x9 step at that size). The
 // history of a small board is short (random 9x9 games end after ~130 plies), so a 2048-bit Bloom
 // filter keeps the false-positive rate (answered by the exact history scan) well under 1 %.
-__host__ __device__ constexpr int bloom_words(int N) { return N <= 9 ? 64 : N <= 13 ? 128 : BBK_GO_BLOOM_WORDS; }
+#ifndef BBK_GO_BLOOM9_WORDS
+#define BBK_GO_BLOOM9_WORDS 64   // Bloom words of boards up to 9x9 (tuning knob; the host asks bbk_go_filter_words)
+#endif
+__host__ __device__ constexpr int bloom_words(int N) { return N <= 9 ? BBK_GO_BLOOM9_WORDS : N <= 13 ? 128 : BBK_GO_BLOOM_WORDS; }
 __host__ __device__ constexpr int pair_words(int N) { return N <= 13 ? 32 : BBK_GO_PAIR_WORDS; }
 __host__ __device__ constexpr int filter_words(int N) { return bloom_words(N) + pair_words(N); }
 __host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
@@ -231,7 +234,8 @@ __device__ __forceinline__ uint32_t run_at(uint32_t X, int s) {
 #ifndef BBK_GO_BLOOM_K
 #define BBK_GO_BLOOM_K 4
 #endif
-constexpr int kBloomK = BBK_GO_BLOOM_K;
+constexpr int kBloomK = BBK_GO_BLOOM_K;   // r02: 4 beat 3, 5 and a 4096-bit 9x9 filter
+static_assert(kBloomK >= 1 && 13 * (kBloomK - 1) < 64, "probe slices must lie inside the 64-bit hash");
 __device__ __forceinline__ uint32_t bloom_idx(uint64_t h, int j, uint32_t M) { return (uint32_t)(h >> (13 * j)) & M; }
 
 template <int N>

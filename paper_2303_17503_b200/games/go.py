@@ -117,8 +117,17 @@ class GoKernel(DeviceKernel):
         self.obs_shape = (size, size, 2 * HISTORY_PLANES + 1)
         self.game_id = f"go_{size}x{size}"
         self.pat_stride = (self.cells + 7) & ~7
-        # superko filter row (u32 words): Bloom + stone-count pairs, sized per board (go.cu filter_words)
-        self.filter_words = (64 if size <= 9 else 128 if size <= 13 else 256) + (32 if size <= 13 else 64)
+
+    @property
+    def filter_words(self) -> int:
+        """u32 words of one env's superko filter row (Bloom + stone-count pairs), as the loaded
+        library sizes it per board (bbk_go_filter_words)."""
+        fw = self.__dict__.get("_filter_words")
+        if fw is None:
+            fw = self._filter_words = int(nat.lib().bbk_go_filter_words(self.size))
+            if fw <= 0:
+                raise UnsupportedGame(f"go size {self.size}: no superko filter layout in the library")
+        return fw
 
     def alloc_private(self, v: DeviceV) -> None:
         torch = _torch()
