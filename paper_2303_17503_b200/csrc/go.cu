@@ -163,12 +163,18 @@ struct WarpSmem {   // one board's scratch (one per segment)
 // read-only path -- one L1 load instead of a chain of ~15 dependent 64-bit multiply / shift ops
 // (go_9x9 +6.7 %); 15x15+ compute it in registers (their shared memory leaves little L1, and the
 // table lost 1.2 % at 19x19).
+#ifndef BBK_GO_ZTABLE_MAX
+#define BBK_GO_ZTABLE_MAX 13   // largest board reading single-point keys from the table
+#endif
+#ifndef BBK_GO_ZROW_MAX
+#define BBK_GO_ZROW_MAX 19     // largest board reading run hashes from the row-prefix table (all)
+#endif
 template <int N>
 __device__ uint64_t g_zob[2 * N * N];
 
 template <int N>
 __device__ __forceinline__ uint64_t zkey(int cell, int colour) {
-    if constexpr (N <= 13) return __ldg(&g_zob<N>[2 * cell + colour]);
+    if constexpr (N <= BBK_GO_ZTABLE_MAX) return __ldg(&g_zob<N>[2 * cell + colour]);
     else return mix64(0x60D00D60C0FFEE00ULL + (uint64_t)N + 2ull * (uint64_t)cell + (uint64_t)colour);
 }
 
@@ -180,7 +186,9 @@ __device__ uint64_t g_zrow[2 * N * (N + 1)];
 
 template <int N>
 __device__ __forceinline__ uint64_t zrun(int row, int s, int len, int colour) {
-    if constexpr (N <= 13) {   // +4 % at 9x9; 19x19 keeps its register-computed keys (table -0.3 %)
+    // r02: +4 % at 9x9; at 19x19 +6 % late game / +2 % over a full cycle (big captured chains), the
+    // single-point key table there stays off (neutral)
+    if constexpr (N <= BBK_GO_ZROW_MAX) {
         const uint64_t* z = g_zrow<N> + (colour * N + row) * (N + 1);
         return __ldg(z + s + len) ^ __ldg(z + s);
     } else {
