@@ -38,9 +38,24 @@ __device__ __constant__ int8_t DR[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
 __device__ __constant__ int8_t DC[8] = {0, -1, 1, -1, 1, 0, -1, 1};
 __device__ __constant__ int8_t OPPD[8] = {5, 7, 6, 4, 3, 0, 2, 1};
 // per type (index = type): step directions and slide directions (owner frame)
-__device__ __constant__ uint8_t STEP[16] = {0, 0x01, 0x00, 0x00, 0xC7, 0x3F, 0x00, 0x00, 0xFF, 0x3F, 0x3F, 0x3F, 0x3F,
-                                            0x39, 0xC6, 0};
-__device__ __constant__ uint8_t SLIDE[16] = {0, 0x00, 0x01, 0x00, 0x00, 0x00, 0xC6, 0x39, 0x00, 0, 0, 0, 0, 0xC6, 0x39, 0};
+constexpr uint8_t STEP_T[16] = {0, 0x01, 0x00, 0x00, 0xC7, 0x3F, 0x00, 0x00, 0xFF, 0x3F, 0x3F, 0x3F, 0x3F, 0x39, 0xC6, 0};
+constexpr uint8_t SLIDE_T[16] = {0, 0x00, 0x01, 0x00, 0x00, 0x00, 0xC6, 0x39, 0x00, 0, 0, 0, 0, 0xC6, 0x39, 0};
+// ... packed 8 types per 64-bit word: a per-lane (divergent) type then indexes registers instead of
+// the constant cache, which serialises distinct addresses (the attack gather reads it 8x per square)
+constexpr uint64_t pack8(const uint8_t* t) {
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; i--) v = (v << 8) | t[i];
+    return v;
+}
+constexpr uint64_t STEP_LO = pack8(STEP_T), STEP_HI = pack8(STEP_T + 8);
+constexpr uint64_t SLIDE_LO = pack8(SLIDE_T), SLIDE_HI = pack8(SLIDE_T + 8);
+static_assert(STEP_LO == 0x00003FC700000100ull && SLIDE_HI == 0x0039C60000000000ull, "type table packing");
+__device__ __forceinline__ uint32_t stepm(int ty) {
+    return (uint32_t)(((ty & 8) ? STEP_HI : STEP_LO) >> ((ty & 7) * 8)) & 0xFFu;
+}
+__device__ __forceinline__ uint32_t slidem(int ty) {
+    return (uint32_t)(((ty & 8) ? SLIDE_HI : SLIDE_LO) >> ((ty & 7) * 8)) & 0xFFu;
+}
 __device__ __constant__ uint8_t HAND_TYPE[7] = {FU, KY, KE, GI, KI, KA, HI};
 __device__ __constant__ uint8_t HCAP[7] = {8, 4, 4, 4, 4, 2, 2};
 __device__ __constant__ uint8_t HOFF[7] = {0, 8, 12, 16, 20, 24, 26};
@@ -113,7 +128,7 @@ __device__ bool attacked(const Acc& at, int t, int w) {
             if (pc) {
                 if (owner(pc) == w) {
                     const int ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
-                    if (((k == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) return true;
+                    if (((k == 1 ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> bit) & 1) return true;
                 }
                 break;
             }
@@ -206,7 +221,7 @@ __device__ void gather_attacks(WarpSmem& S, int lane) {
             const bool adj = lower ? bpos == pos - 1 : bpos == pos + 1;
             const uint8_t pc = bd[q];
             const int w = owner(pc), ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
-            if (((adj ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> bit) & 1) {
+            if (((adj ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> bit) & 1) {
                 if (w == 0) { m0 |= 1u << (ty - 1); n0++; } else { m1 |= 1u << (ty - 1); n1++; }
             }
         }
@@ -473,11 +488,11 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                     if (own < 0) {
                         if (owner(pc) == 0) own = s;
                         else {
-                            if (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> d) & 1) { checker = true; block = ray; }
+                            if (((kk == 1 ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> d) & 1) { checker = true; block = ray; }
                             break;
                         }
                     } else {
-                        if (owner(pc) == 1 && ((SLIDE[ty] >> d) & 1)) { pin = (int8_t)own; pray = ray; }
+                        if (owner(pc) == 1 && ((slidem(ty) >> d) & 1)) { pin = (int8_t)own; pray = ray; }
                         break;
                     }
                 }
@@ -500,7 +515,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                     ok = true;
                     while (son(xr, xc)) {
                         const uint8_t pc = bd[xr * 9 + xc];
-                        if (pc) { ok = !(owner(pc) == 1 && ((SLIDE[ptype(pc)] >> od) & 1)); break; }
+                        if (pc) { ok = !(owner(pc) == 1 && ((slidem(ptype(pc)) >> od) & 1)); break; }
                         xr += DR[od]; xc += DC[od];
                     }
                 }
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                 const int sq = lane + 32 * j;
                 const uint8_t pc = sq < 81 ? bd[sq] : (uint8_t)0;
                 const int ty = ptype(pc);
-                dirs[j] = (!pc || owner(pc) != 0 || ty == OU) ? 0u : ty == KE ? 0x300u : (uint32_t)(STEP[ty] | SLIDE[ty]);
+                dirs[j] = (!pc || owner(pc) != 0 || ty == OU) ? 0u : ty == KE ? 0x300u : (uint32_t)(stepm(ty) | slidem(ty));
                 mine += __popc(dirs[j]);
             }
             int incl = mine;
@@ -571,7 +586,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                     }
                     continue;
                 }
-                const bool slide = (SLIDE[ty] >> d) & 1;
+                const bool slide = (slidem(ty) >> d) & 1;
                 int rr = r + DR[d], cc = c + DC[d];
                 while (son(rr, cc)) {
                     const int to = rr * 9 + cc;
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 6
                             const uint8_t pc = bd[rr * 9 + cc];
                             if (pc) {
                                 const int ty = ptype(pc);
-                                if (owner(pc) == 1 && ty != OU && (((kk == 1 ? (STEP[ty] | SLIDE[ty]) : SLIDE[ty]) >> d) & 1))
+                                if (owner(pc) == 1 && ty != OU && (((kk == 1 ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> d) & 1))
                                     from = rr * 9 + cc;
                                 break;
                             }
