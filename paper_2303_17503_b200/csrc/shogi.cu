@@ -180,17 +180,58 @@ __device__ __forceinline__ uint64_t sq_key(uint8_t pc, int s) {
     return mix64(0x5306100000000000ULL + (uint64_t)pc * 128 + (uint64_t)s);
 }
 
-// Occupancy bit masks of the 52 lines of the board (one lane per line).
-__device__ void build_lines(WarpSmem& S, int lane) {
-    for (int j = lane; j < 52; j += 32) {
-        uint32_t m = 0u;
-#pragma unroll
-        for (int i = 0; i < 9; i++) {
-            const int r = j < 9 ? j : i;
-            const int c = j < 9 ? i : j < 18 ? j - 9 : j < 35 ? i - (j - 18) + 8 : (j - 35) - i;
-            if ((unsigned)c < 9u && S.bd[r * 9 + c]) m |= 1u << i;
+// Occupancy bit masks of the 52 lines of the board. The squares are listed in four orders (rows,
+// columns, diagonals r - c = k - 8, anti-diagonals r + c = k; each line contiguous, its squares by
+// increasing row within a diagonal); three ballots per order give the occupancy as a 96-bit stream
+// in that order, and lane j cuts line j out of its stream with one funnel shift (instead of nine
+// byte loads and index arithmetic per line).
+struct LineOrder {
+    uint8_t sq[4][96];      // square at position o of order q (o >= 81: padding)
+    uint8_t start[52], len[52], r0[52];   // line j: stream offset, length, row of its first bit
+};
+constexpr LineOrder make_line_order() {
+    LineOrder t{};
+    int o = 0;
+    for (int r = 0; r < 9; r++)
+        for (int c = 0; c < 9; c++) t.sq[0][o++] = (uint8_t)(r * 9 + c);
+    o = 0;
+    for (int c = 0; c < 9; c++)
+        for (int r = 0; r < 9; r++) t.sq[1][o++] = (uint8_t)(r * 9 + c);
+    for (int j = 0; j < 18; j++) { t.start[j] = (uint8_t)(9 * (j % 9)); t.len[j] = 9; t.r0[j] = 0; }
+    for (int q = 2; q < 4; q++) {
+        o = 0;
+        for (int k = 0; k < 17; k++) {
+            const int lo = k - 8 > 0 ? k - 8 : 0, hi = k < 8 ? k : 8;
+            const int j = (q == 2 ? 18 : 35) + k;
+            t.start[j] = (uint8_t)o; t.len[j] = (uint8_t)(hi - lo + 1); t.r0[j] = (uint8_t)lo;
+            for (int r = lo; r <= hi; r++) t.sq[q][o++] = (uint8_t)(r * 9 + (q == 2 ? r - k + 8 : k - r));
         }
-        S.line[j] = (uint16_t)m;
+    }
+    return t;
+}
+__device__ const LineOrder g_lines = make_line_order();
+
+__device__ void build_lines(WarpSmem& S, int lane) {
+    uint32_t w[4][3];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const int o = lane + 32 * k;
+            const bool occ = o < 81 && S.bd[__ldg(&g_lines.sq[q][o])] != 0;
+            w[q][k] = __ballot_sync(BBK_FULL, occ);
+        }
+    for (int j = lane; j < 52; j += 32) {
+        const int q = j < 9 ? 0 : j < 18 ? 1 : j < 35 ? 2 : 3;
+        const int st = __ldg(&g_lines.start[j]), ln = __ldg(&g_lines.len[j]), r0 = __ldg(&g_lines.r0[j]);
+        const int wi = st >> 5;
+        // select the order's words without a dynamically indexed register array
+        const uint32_t a0 = q == 0 ? w[0][0] : q == 1 ? w[1][0] : q == 2 ? w[2][0] : w[3][0];
+        const uint32_t a1 = q == 0 ? w[0][1] : q == 1 ? w[1][1] : q == 2 ? w[2][1] : w[3][1];
+        const uint32_t a2 = q == 0 ? w[0][2] : q == 1 ? w[1][2] : q == 2 ? w[2][2] : w[3][2];
+        const uint32_t lo = wi == 0 ? a0 : wi == 1 ? a1 : a2, hi = wi == 0 ? a1 : wi == 1 ? a2 : 0u;
+        const uint32_t m = __funnelshift_r(lo, hi, st & 31) & ((1u << ln) - 1u);
+        S.line[j] = (uint16_t)(m << r0);
     }
 }
 
