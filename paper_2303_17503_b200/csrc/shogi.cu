@@ -262,9 +262,11 @@ __device__ void gather_attacks(WarpSmem& S, int lane) {
             const bool adj = lower ? bpos == pos - 1 : bpos == pos + 1;
             const uint8_t pc = bd[q];
             const int w = owner(pc), ty = ptype(pc), bit = w == 0 ? OPPD[d] : d;
-            if (((adj ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> bit) & 1) {
-                if (w == 0) { m0 |= 1u << (ty - 1); n0++; } else { m1 |= 1u << (ty - 1); n1++; }
-            }
+            // branch-free update (the owner / hit pattern differs lane to lane)
+            const uint32_t hit = ((adj ? (stepm(ty) | slidem(ty)) : slidem(ty)) >> bit) & 1u;
+            const uint32_t tb = hit << ((ty - 1) & 15), h0 = hit & (uint32_t)(w == 0), h1 = hit & (uint32_t)(w != 0);
+            m0 |= w == 0 ? tb : 0u; m1 |= w != 0 ? tb : 0u;
+            n0 += h0; n1 += h1;
         }
         for (int dc = -1; dc <= 1; dc += 2) {
             if (son(r + 2, c + dc) && bd[(r + 2) * 9 + c + dc] == KE) { m0 |= 1u << (KE - 1); n0++; }
