@@ -32,6 +32,10 @@
 #include "../../include/bbk.h"
 
 namespace go {
+#ifndef BBK_GO_OBS_UNROLL
+#define BBK_GO_OBS_UNROLL 2
+#endif
+constexpr int kGoObsUnroll = BBK_GO_OBS_UNROLL;   // observation chunk loop unroll (tuning knob)
 using namespace bbk;
 
 constexpr int kWarps = 4;             // warps per CTA
@@ -566,7 +570,7 @@ __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, flo
         const uint32_t q0 = (uint32_t)(head + 8 * sl), sh = q0 & 31u;
         const uint32_t* wp = W + (q0 >> 5);
         BBK_CHECK(nchunk <= 0 || (head + 8 * (nchunk - 1)) / 32 + 1 <= NW);   // last chunk's words are staged
-#pragma unroll 2
+#pragma unroll kGoObsUnroll
         for (int j = sl; j < nchunk; j += L, wp += L / 4) {
             const uint32_t t = __funnelshift_r(wp[0], wp[1], sh);
             const float4 lo = lut[t & 15u], hi = lut[(t >> 4) & 15u];
