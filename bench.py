@@ -372,6 +372,11 @@ def game_block(args, game, dev):
     del loop
     out = {"value": B * K / (ms / 1e3), "unit": "env-steps/s", "batch": B, "steps": K, "warmup": W,
            "ms_per_step": ms / K, "roofline": roofline(game, B, kern_ms, ms / K), "gpu_launches": K}
+    if not args.no_sweep:   # batch sizes 2^10..2^17 (north star), as for the headline game
+        from paper_2303_17503_b200.core import resolve
+
+        gdef = resolve(game)
+        out["sweep"] = run_sweep(args, gdef, gdef.batch_kernel, dev, 0)
     if not args.no_e2e:
         sub = argparse.Namespace(**{**vars(args), "steps": K, "warmup": W})
         out["e2e"] = run_e2e(sub, game, dev, 1, 0, B)
