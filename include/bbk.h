@@ -34,8 +34,9 @@
 extern "C" {
 #endif
 
-#define BBK_ABI_VERSION 5   /* 3: bbk_go_state.lab, fingerprints, small engines; 4: batched UCT search;
-                               5: per-size Go superko filters (bbk_go_filter_words, size arg of bbk_go_rebuild_bloom) */
+#define BBK_ABI_VERSION 6   /* 3: fingerprints, small engines; 4: batched UCT search;
+                               5: per-size Go superko filters (bbk_go_filter_words, size arg of bbk_go_rebuild_bloom);
+                               6: Go chain labels moved from bbk_go_state to the in-place bbk_go_store, bbk_go_relabel */
 
 typedef struct bbk_cols {
     float*    observation;        /* may be NULL: skip observation emission */
@@ -62,8 +63,10 @@ typedef struct bbk_cols {
  * observe :264-273, Core.encode :103-111.
  *   pat[n, pat_stride]  uint16: bit 2t / 2t+1 = black / white stone at the
  *                       point in boards_hist[t] (t = 0 newest .. 7)
- *   lab[n, pat_stride]  uint16: chain label per stone = one point of the stone's chain
- *                       (maintained incrementally; values at empty points are don't-care)
+ *   store.lab[n, pat_stride] uint16: chain label per stone = one point of the stone's chain,
+ *                       maintained IN PLACE along a lineage like the history (a step writes only
+ *                       the labels it changes; values at empty points are never read), rebuilt
+ *                       from a batch's board by bbk_go_relabel when that batch branches
  *   history[n, hist_cap] uint64 append-only superko hashes (history set)
  *   bloom[n, bbk_go_filter_words(size)] uint32: a Bloom filter over history hashes, then a
  *                        filter of the (black, white) stone-count pairs of the history
@@ -77,7 +80,6 @@ typedef struct bbk_cols {
 
 typedef struct bbk_go_state {
     uint16_t* pat;
-    uint16_t* lab;      /* [n, pat_stride] chain label of every stone (a point of its chain) */
     uint64_t* hash;
     uint64_t* hist_xor;
     int32_t*  hist_len;
@@ -88,6 +90,7 @@ typedef struct bbk_go_state {
 typedef struct bbk_go_store {
     uint64_t* history;
     uint32_t* bloom;
+    uint16_t* lab;      /* [n, pat_stride] chain label of every stone (a point of its chain), in place */
     int32_t   hist_cap;
 } bbk_go_store;
 
@@ -113,6 +116,9 @@ int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* ob
 
 /* Rebuild Bloom filters from history[0:hist_len) (used when a batch branches). */
 int bbk_go_rebuild_bloom(int size, const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream);
+/* Rebuild the chain labels of store.lab from each board's current position (bits 0/1 of pat):
+ * label = the lowest point of the chain. Used with bbk_go_rebuild_bloom when a batch branches. */
+int bbk_go_relabel(int size, const bbk_go_store* store, const uint16_t* pat, int64_t n, void* stream);
 
 /* ---------------------------------------------------------- Backgammon --
  * Replaces games/backgammon.py: _legal_mask :62-95, _roll :125-130,

@@ -11,7 +11,9 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("BBK_LIB") or os.path.join(_PKG, "_lib", "libbbk.so")   # BBK_LIB: A/B builds
+# BBK_LIB: A/B or checked builds (made absolute: subprocesses, e.g. the reference hook-in run, may
+# start in another directory)
+LIB_PATH = os.path.abspath(os.environ["BBK_LIB"]) if os.environ.get("BBK_LIB") else os.path.join(_PKG, "_lib", "libbbk.so")
 
 _lock = threading.Lock()
 _lib = None
@@ -38,12 +40,12 @@ class Cols(C.Structure):
 
 
 class GoState(C.Structure):
-    _fields_ = [("pat", P), ("lab", P), ("hash", P), ("hist_xor", P), ("hist_len", P), ("role_to_move", P),
+    _fields_ = [("pat", P), ("hash", P), ("hist_xor", P), ("hist_len", P), ("role_to_move", P),
                 ("pass_count", P)]
 
 
 class GoStore(C.Structure):
-    _fields_ = [("history", P), ("bloom", P), ("hist_cap", I32)]
+    _fields_ = [("history", P), ("bloom", P), ("lab", P), ("hist_cap", I32)]
 
 
 class BgState(C.Structure):
@@ -101,6 +103,7 @@ def _declare(L):
     sig("bbk_go_observe", [C.c_int, P, P, P, I64, P])
     sig("bbk_go_filter_words", [C.c_int])
     sig("bbk_go_rebuild_bloom", [C.c_int, ptr(GoStore), P, I64, P])
+    sig("bbk_go_relabel", [C.c_int, ptr(GoStore), P, I64, P])
     sig("bbk_bg_init", [ptr(Cols), ptr(BgState), I64, I64, U64, P, I32, P])
     sig("bbk_bg_step", [ptr(Cols), ptr(BgState), ptr(Cols), ptr(BgState), P, I64, I64, U64, P, I32, P])
     sig("bbk_bg_observe", [ptr(BgState), P, P, I64, P])

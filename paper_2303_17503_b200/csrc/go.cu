@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                 }
             } else {
                 const uint4* src = reinterpret_cast<const uint4*>(p.in_s.pat + b * (int64_t)PS);
-                const uint4* lsrc = reinterpret_cast<const uint4*>(p.in_s.lab + b * (int64_t)PS);
+                const uint4* lsrc = reinterpret_cast<const uint4*>(p.store.lab + b * (int64_t)PS);
                 for (int i = sl; i < PS / 8; i += L) {
                     take(i, src[i]);
                     reinterpret_cast<uint4*>(lab)[i] = lsrc[i];
@@ -841,14 +841,23 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
                     const uint32_t lr = (ca < N - 1 && ((Mr >> (ca + 1)) & 1u)) ? lab[a + 1] : NONE;
                     const uint32_t L0 = lu != NONE ? lu : ld != NONE ? ld : ll != NONE ? ll : lr != NONE ? lr : (uint32_t)a;
                     g.sync();
+                    // labels change only here: the in-place store row takes the same writes (a few
+                    // bytes per step instead of the whole row)
+                    uint16_t* glab = p.store.lab + b * (int64_t)PS;
                     if ((ld != NONE && ld != L0) | (ll != NONE && ll != L0) | (lr != NONE && lr != L0)) {
                         for (uint32_t m_ = M; m_; m_ &= m_ - 1) {   // lanes >= N hold no stones
                             const int cell = sl * N + __ffs(m_) - 1;
                             const uint32_t l = lab[cell];
-                            if (l == ld || l == ll || l == lr) lab[cell] = (uint16_t)L0;
+                            if (l == ld || l == ll || l == lr) {
+                                lab[cell] = (uint16_t)L0;
+                                glab[cell] = (uint16_t)L0;
+                            }
                         }
                     }
-                    if (sl == 0) lab[a] = (uint16_t)L0;
+                    if (sl == 0) {
+                        lab[a] = (uint16_t)L0;
+                        glab[a] = (uint16_t)L0;
+                    }
                     g.sync();
                 }
                 if (sl == ra) M |= 1u << ca;
@@ -930,11 +939,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             }
         }
         g.sync();
-        uint16_t* olab = p.out_s.lab + b * (int64_t)PS;
-        for (int i = sl; i < PS / 8; i += L) {
+        for (int i = sl; i < PS / 8; i += L)
             reinterpret_cast<uint4*>(opat)[i] = reinterpret_cast<const uint4*>(S.pat)[i];
-            reinterpret_cast<uint4*>(olab)[i] = reinterpret_cast<const uint4*>(lab)[i];
-        }
         const bool truncated = !terminal && step >= p.max_steps;
         // legal mask of the new mover (skipped once the slot is finished)
         uint32_t legal = 0u;
@@ -989,7 +995,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
             else pf_raw = load_field(fref, nb);
             const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pat_pf);
             const char* src = reinterpret_cast<const char*>(p.in_s.pat + nb * (int64_t)PS);
-            const char* lsrc = reinterpret_cast<const char*>(p.in_s.lab + nb * (int64_t)PS);
+            const char* lsrc = reinterpret_cast<const char*>(p.store.lab + nb * (int64_t)PS);
             for (int i = sl; i < PS / 8; i += L) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src + 16 * i));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 2u * PS + 16u * i), "l"(lsrc + 16 * i));
@@ -1067,6 +1073,48 @@ __global__ void rebuild_bloom_kernel(bbk_go_store st, const int32_t* hist_len, i
         // history keeps no stone counts: mark every pair as seen (correct, only slower)
         for (int i = BW + lane; i < FW; i += 32) st.bloom[b * FW + i] = 0xFFFFFFFFu;
         __syncwarp();
+    }
+}
+
+// Chain labels of each board's current position (bits 0 / 1 of pat), label = the chain's lowest
+// point, into the in-place store row: one warp per board, lane = row, one bit-parallel flood per chain.
+template <int N>
+__global__ void relabel_kernel(bbk_go_store st, const uint16_t* pat, int64_t n) {
+    constexpr int PS = pat_stride(N);
+    constexpr uint32_t ROW = (1u << N) - 1u;
+    const Seg<32> g;
+    const int lane = g.sl;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    for (int64_t b = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); b < n; b += nwarps) {
+        const uint16_t* pb = pat + b * (int64_t)PS;
+        uint16_t* lb = st.lab + b * (int64_t)PS;
+        uint32_t rows[2] = {0u, 0u};
+        if (lane < N)
+            for (int c = 0; c < N; c++) {
+                const uint32_t v = pb[lane * N + c];
+                rows[0] |= (v & 1u) << c;
+                rows[1] |= ((v >> 1) & 1u) << c;
+            }
+#pragma unroll
+        for (int col = 0; col < 2; col++) {
+            uint32_t left = rows[col];   // stones of this colour not labelled yet
+            while (g.any(left != 0u)) {
+                const unsigned who = g.ballot(left != 0u);
+                const int r0 = __ffs(who) - 1;                    // lowest row with an unlabelled stone
+                const uint32_t lr = g.shfl(left, r0);
+                const int label = r0 * N + __ffs(lr) - 1;        // its lowest point
+                uint32_t F = lane == r0 ? (lr & (0u - lr)) : 0u;
+                while (true) {
+                    const uint32_t F2 = (F | dilate<N>(g, F)) & rows[col];
+                    const bool ch = g.any(F2 != F);
+                    F = F2;
+                    if (!ch) break;
+                }
+                for (uint32_t f_ = F; f_; f_ &= f_ - 1) lb[lane * N + __ffs(f_) - 1] = (uint16_t)label;
+                left &= ~F;
+            }
+        }
+        (void)ROW;
     }
 }
 
@@ -1203,6 +1251,26 @@ int bbk_go_observe(int size, const uint16_t* pat, const uint8_t* role, float* ob
         case 19: return go::launch_observe<19>(pat, role, obs, n, (cudaStream_t)stream);
         default: return (int)cudaErrorInvalidValue;
     }
+}
+
+int bbk_go_relabel(int size, const bbk_go_store* store, const uint16_t* pat, int64_t n, void* stream) {
+    if (n <= 0) return 0;
+    int64_t grid = (n + go::kWarps - 1) / go::kWarps;
+    if (grid > 148 * 8) grid = 148 * 8;
+    const dim3 g((unsigned)grid), t(go::kWarps * 32);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (size) {
+        case 5: go::relabel_kernel<5><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 7: go::relabel_kernel<7><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 9: go::relabel_kernel<9><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 11: go::relabel_kernel<11><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 13: go::relabel_kernel<13><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 15: go::relabel_kernel<15><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 17: go::relabel_kernel<17><<<g, t, 0, s>>>(*store, pat, n); break;
+        case 19: go::relabel_kernel<19><<<g, t, 0, s>>>(*store, pat, n); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    return (int)cudaGetLastError();
 }
 
 int bbk_go_rebuild_bloom(int size, const bbk_go_store* store, const int32_t* hist_len, int64_t n, void* stream) {

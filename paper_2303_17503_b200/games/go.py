@@ -74,27 +74,36 @@ class GoCoreView:
 
 
 class GoStore:
-    """Append-only per-env superko history + Bloom filter shared along a lineage."""
+    """Per-env state shared IN PLACE along a lineage: the append-only superko history, its Bloom /
+    stone-count filter, and the chain labels of the lineage head's board (a step writes only the
+    labels it changes; a branch rebuilds them from the branching batch's board, bbk_go_relabel)."""
 
-    def __init__(self, history, bloom, hist_cap: int):
+    def __init__(self, history, bloom, lab, hist_cap: int):
         self.history = history
         self.bloom = bloom
+        self.lab = lab
         self.hist_cap = hist_cap
         self.lineage = None
 
     def row_tensors(self):
-        return [self.history, self.bloom]
+        return [self.history, self.bloom, self.lab]
 
     def like(self, n: int) -> "GoStore":
         torch = _torch()
         return GoStore(torch.empty((n, self.hist_cap), dtype=torch.int64, device=self.history.device),
                        torch.empty((n,) + tuple(self.bloom.shape[1:]), dtype=self.bloom.dtype,
-                                   device=self.bloom.device), self.hist_cap)
+                                   device=self.bloom.device),
+                       torch.empty((n,) + tuple(self.lab.shape[1:]), dtype=self.lab.dtype, device=self.lab.device),
+                       self.hist_cap)
+
+    def clone_rows(self, rows=slice(None)) -> "GoStore":
+        return GoStore(self.history[rows].clone(), self.bloom[rows].clone(), self.lab[rows].clone(), self.hist_cap)
 
     def struct(self) -> nat.GoStore:
         st = self.__dict__.get("_struct")
         if st is None:
-            st = self._struct = nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), self.hist_cap)
+            st = self._struct = nat.GoStore(nat.ptr(self.history), nat.ptr(self.bloom), nat.ptr(self.lab),
+                                            self.hist_cap)
         return st
 
 
@@ -134,7 +143,6 @@ class GoKernel(DeviceKernel):
         n, dev = v.n, v.device
         p = v.priv
         p.pat = torch.empty((n, self.pat_stride), dtype=torch.int16, device=dev)
-        p.lab = torch.empty((n, self.pat_stride), dtype=torch.int16, device=dev)
         p.hash = torch.empty(n, dtype=torch.int64, device=dev)
         p.hist_xor = torch.empty(n, dtype=torch.int64, device=dev)
         p.hist_len = torch.empty(n, dtype=torch.int32, device=dev)
@@ -146,7 +154,7 @@ class GoKernel(DeviceKernel):
         if st is not None:
             return st
         p = v.priv
-        st = v._gostate = nat.GoState(nat.ptr(p.pat), nat.ptr(p.lab), nat.ptr(p.hash), nat.ptr(p.hist_xor),
+        st = v._gostate = nat.GoState(nat.ptr(p.pat), nat.ptr(p.hash), nat.ptr(p.hist_xor),
                                       nat.ptr(p.hist_len), nat.ptr(p.role_to_move), nat.ptr(p.pass_count))
         return st
 
@@ -155,7 +163,8 @@ class GoKernel(DeviceKernel):
         cap = int(limit) + 2
         hist = torch.empty((n, cap), dtype=torch.int64, device=device)
         bloom = torch.empty((n, self.filter_words), dtype=torch.int32, device=device)
-        return GoStore(hist, bloom, cap)
+        lab = torch.empty((n, self.pat_stride), dtype=torch.int16, device=device)   # written before read
+        return GoStore(hist, bloom, lab, cap)
 
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
         v.store = self.new_store(v.n, v.limit, v.device)
@@ -167,10 +176,13 @@ class GoKernel(DeviceKernel):
     branch_keep = 2   # a live slot's history prefix survives two batch steps (see history_of)
 
     def rebuild_filters(self, w: DeviceV) -> None:
-        """Recompute the Bloom / count-pair filters of w's store from its history prefixes
-        (bbk_go_rebuild_bloom): after a branch copied a store that later steps may have added to."""
-        nat.check(nat.lib().bbk_go_rebuild_bloom(self.size, w.store.struct(), nat.ptr(w.priv.hist_len), w.n,
-                                                 nat.stream_handle(w.device)), "bbk_go_rebuild_bloom")
+        """Recompute w's store from w's own state after a branch copied a store that later steps may
+        have changed: the Bloom / count-pair filters from its history prefixes (bbk_go_rebuild_bloom)
+        and the chain labels from its board (bbk_go_relabel)."""
+        st, stream = w.store.struct(), nat.stream_handle(w.device)
+        nat.check(nat.lib().bbk_go_rebuild_bloom(self.size, st, nat.ptr(w.priv.hist_len), w.n, stream),
+                  "bbk_go_rebuild_bloom")
+        nat.check(nat.lib().bbk_go_relabel(self.size, st, nat.ptr(w.priv.pat), w.n, stream), "bbk_go_relabel")
 
     def prepare_step(self, v: DeviceV, out: DeviceV) -> None:
         store = v.store
@@ -181,7 +193,7 @@ class GoKernel(DeviceKernel):
             # branch: private copy of the history, filters rebuilt for v's lengths; the
             # original lineage keeps its store (and stays steppable)
             old = store.lineage
-            store = GoStore(store.history.clone(), store.bloom.clone(), store.hist_cap)
+            store = store.clone_rows()
             store.lineage = Lineage(v.uid, v.t, old.append_only)
             self.rebuild_filters(_with_store(v, store))
         out.store = store
@@ -211,7 +223,7 @@ class GoKernel(DeviceKernel):
     def slice_store(self, v: DeviceV, w: DeviceV, i: int) -> None:
         depth = self.branch_depth(v)
         s = v.store
-        w.store = GoStore(s.history[i:i + 1].clone(), s.bloom[i:i + 1].clone(), s.hist_cap)
+        w.store = s.clone_rows(slice(i, i + 1))
         w.store.lineage = Lineage(w.uid, w.t)
         if depth > 0:
             self.rebuild_filters(w)

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     L = _native.lib()
     missing = [s for s in declared_symbols() if not hasattr(L, s)]
     assert not missing, missing
-    assert L.bbk_abi_version() == 5
+    assert L.bbk_abi_version() == 6
     from paper_2303_17503_b200.games.go import GoKernel
 
     for n in (5, 7, 9, 11, 13, 15, 17, 19):   # host allocation == kernel row stride

@@ -34,7 +34,7 @@ def test_history_overflow_is_reported():
 
     def shrunk(vv, o, *args):   # launch with a 3-entry history declared over the full-size tensor
         s = o.store
-        o.store = go.GoStore(s.history, s.bloom, 3)
+        o.store = go.GoStore(s.history, s.bloom, s.lab, 3)
         try:
             real(vv, o, *args)
         finally:

@@ -42,6 +42,8 @@ def test_reference_suite_through_the_device_plugin():
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([REF, ROOT, env.get("PYTHONPATH", "")])
     env["PYTHONDONTWRITEBYTECODE"] = "1"
+    if env.get("BBK_LIB"):   # the subprocess runs in the reference's test directory
+        env["BBK_LIB"] = os.path.join(ROOT, env["BBK_LIB"]) if not os.path.isabs(env["BBK_LIB"]) else env["BBK_LIB"]
     cmd = [sys.executable, "-m", "pytest", "-p", "paper_2303_17503_b200.reference_plugin", "-p", "no:cacheprovider",
            "-q", "-rA", "--rootdir", TESTS] + [os.path.join(TESTS, s) for s in SELECTION]
     r = subprocess.run(cmd, cwd=TESTS, env=env, capture_output=True, text=True, timeout=1500)
