@@ -413,7 +413,10 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
 // (bbk_chess_load, the device twin of the oracle's orc_chess_set_fen test hook); a separate
 // instantiation so the hot kernel's code is unchanged.
 template <bool kLoad>
-__global__ void __launch_bounds__(kWarps * 32, 9) step_kernel(Params p) {   // 56 registers, no spills
+#ifndef BBK_CHESS_MIN_CTAS
+#define BBK_CHESS_MIN_CTAS 9
+#endif
+__global__ void __launch_bounds__(kWarps * 32, BBK_CHESS_MIN_CTAS) step_kernel(Params p) {   // 56 registers, no spills
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {

@@ -408,7 +408,10 @@ __device__ __forceinline__ void issue_prefetch(WarpSmem& S, const Params& p, int
 // (bbk_shogi_load, the device twin of the oracle's orc_shogi_set_sfen test hook); a separate
 // instantiation so the hot kernel's code is unchanged.
 template <bool kLoad>
-__global__ void __launch_bounds__(kWarps * 32, 8) step_kernel(Params p) {   // 64 registers: 8 CTAs per SM
+#ifndef BBK_SHOGI_MIN_CTAS
+#define BBK_SHOGI_MIN_CTAS 9   // r02 (after the grid / line / unroll changes): 9 = +1.7 % over 8 (56 registers), 10: -6 %
+#endif
+__global__ void __launch_bounds__(kWarps * 32, BBK_SHOGI_MIN_CTAS) step_kernel(Params p) {
     __shared__ WarpSmem sm[kWarps];
     __shared__ float4 lut[16];
     if (threadIdx.x < 16) {
