@@ -652,7 +652,10 @@ __device__ __forceinline__ uint64_t load_field(const FieldRefWide& f, int64_t b)
 }
 // deferred decode for the small boards (+1 % at 9x9); 19x19 decodes at the load (the extra live
 // register across the board cost 1.7 % there)
-template <int N> constexpr bool kDeferFields = N <= 13;
+#ifndef BBK_GO_DEFER_MAX
+#define BBK_GO_DEFER_MAX 13
+#endif
+template <int N> constexpr bool kDeferFields = N <= BBK_GO_DEFER_MAX;
 
 __device__ __forceinline__ FieldRef field_ref(const StepParams& p, int lane) {
     switch (lane) {
