@@ -73,7 +73,7 @@ def parse(argv=None):
                     help="strong scaling: total envs split over the ranks (BASELINE config 5: backgammon 2^17)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="bounded CPU baseline sample length")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="omit the batch-size sweep 2^10..2^17 from the line")

@@ -688,10 +688,10 @@ __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
 // the placement's neighbour loop: rolled up for the small boards (smaller hot code, +0.7 % at 9x9)
 constexpr int kNbUnroll = BBK_GO_NB_UNROLL;
 
-// resident CTAs per SM the register budget is sized for: small boards fit 8 (shared memory allows it)
 #ifndef BBK_GO_GRID_BOARDS
 #define BBK_GO_GRID_BOARDS -1   // boards per warp segment per launch: 0 persistent, -1 per-size default
 #endif
+// resident CTAs per SM the register budget is sized for: small boards fit 8 (shared memory allows it)
 #ifndef BBK_GO_CTAS_SMALL
 #define BBK_GO_CTAS_SMALL 8
 #endif
