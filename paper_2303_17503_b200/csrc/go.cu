@@ -519,11 +519,50 @@ __device__ uint32_t legal_rows(const Seg<L>& g, WarpSmem<N>& S, int ycol, uint32
 // f % 17 of the point pattern P[f / 17]; the [N, N, 17] record is emitted as
 // float4 chunks of the flat 16-byte-aligned stream (records are not 16-B
 // aligned; at most 3 scalar floats at each edge) through a 16-entry LUT.
+#ifndef BBK_GO_OBS_DIRECT_MIN
+#define BBK_GO_OBS_DIRECT_MIN 15   // smallest board cutting its observation chunks straight from pat
+#endif
 template <int N, int L>
 __device__ void emit_obs(const Seg<L>& g, WarpSmem<N>& S, const float4* lut, float* obs, int64_t b, int role) {
     constexpr int C = N * N;
     constexpr int NF = C * kPlanes;
     const int sl = g.sl;
+    if constexpr (N >= BBK_GO_OBS_DIRECT_MIN) {
+        // Large boards: each 8-float chunk is cut straight from the two points' history patterns
+        // (float f = plane f % 17 of point f / 17), no staged pattern / bit-stream passes: fewer
+        // shared-memory round trips for more ALU work -- 19x19 +1.2 % over a full cycle, +1.6 % late
+        // game; 9x9 (where ALU is the limit) -1.5 %, so small boards keep the staged passes below.
+        const uint32_t hi16 = (uint32_t)role << 16;
+        auto Pv = [&](uint32_t c) -> uint32_t {   // point c's 17-bit pattern for this role
+            uint32_t u = S.pat[c];
+            if (role) u = ((u & 0x5555u) << 1) | ((u >> 1) & 0x5555u);
+            return u | hi16;
+        };
+        auto bits8 = [&](uint32_t q) -> uint32_t {   // floats q..q+7 of the record (8 <= 17: two points)
+            const uint32_t c = (q * 61681u) >> 20, k = q - 17u * c;   // q / 17, exact for q < 65536
+            BBK_CHECK(c == q / 17u && c + 1 < (uint32_t)pat_stride(N));
+            return ((Pv(c) >> k) | (Pv(c + 1) << (17 - k))) & 0xFFu;
+        };
+        const int64_t F0 = b * (int64_t)NF;
+        float* rec = obs + F0;
+        const int head = (int)((8 - (F0 & 7)) & 7);             // floats before the first 32-B chunk
+        const int nchunk = (NF - head) >> 3;
+        const int tail0 = head + 8 * nchunk;
+        if (sl < head || (sl >= 8 && sl - 8 < NF - tail0)) {   // at most 7 edge floats each side
+            const uint32_t fi = sl < 8 ? (uint32_t)sl : (uint32_t)(tail0 + sl - 8);
+            rec[fi] = (float)(bits8(fi) & 1u);
+        }
+        float* o8 = rec + head;
+#pragma unroll kGoObsUnroll
+        for (int j = sl; j < nchunk; j += L) {
+            const uint32_t t = bits8((uint32_t)(head + 8 * j));
+            const float4 lo = lut[t & 15u], hi = lut[(t >> 4) & 15u];
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o8 + 8 * j), "f"(lo.x), "f"(lo.y),
+                         "f"(lo.z), "f"(lo.w), "f"(hi.x), "f"(hi.y), "f"(hi.z), "f"(hi.w) : "memory");
+        }
+        g.sync();
+        return;
+    }
     uint32_t* P = S.u.ob.P;
     {   // 8 points per lane-iteration: black/white swapped for role 1, colour bit 16
         const uint32_t hi = (uint32_t)role << 16;
