@@ -419,6 +419,7 @@ def run_e2e(args, game, dev, world, slot0, B):
     from paper_2303_17503_b200.agents import random_actions_device
     from paper_2303_17503_b200.core import Batch, batch_step, resolve
     from paper_2303_17503_b200.games._device import ZERO_COPY
+    from paper_2303_17503_b200.session import ResultFetcher
 
     gdef = resolve(game)
     kern = gdef.batch_kernel
@@ -427,18 +428,9 @@ def run_e2e(args, game, dev, world, slot0, B):
                                                             device=dev, next_key=root.child(1)))
     acts = [torch.empty(B, dtype=torch.int64, pin_memory=True) for _ in range(2)]
     P = gdef.spec.num_players
-    host = [dict(r=torch.empty((B, P), dtype=torch.float32, pin_memory=True),
-                 term=torch.empty(B, dtype=torch.bool, pin_memory=True),
-                 trunc=torch.empty(B, dtype=torch.bool, pin_memory=True),
-                 cp=torch.empty(B, dtype=torch.int32, pin_memory=True)) for _ in range(2)]
-    main = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    pending = []      # (batch whose results are in flight, copy-stream event, host buffer set)
+    fetcher = ResultFetcher(B, P, dev)   # public API: pinned double buffers, one native call per step
     t = 0
     acts[0].copy_(random_actions_device(batch, root.child(1)))
-
-    def read(entry):
-        entry[1].synchronize()    # step t's rewards / flags / current player are now in host memory
 
     def one():
         nonlocal batch, t
@@ -447,29 +439,14 @@ def run_e2e(args, game, dev, world, slot0, B):
                            next_actions=acts[(t + 1) % 2] if ZERO_COPY else None)
         if not ZERO_COPY:
             acts[(t + 1) % 2].copy_(random_actions_device(batch, nk), non_blocking=True)
-        d = batch.device
-        h = host[t % 2]
-        done = torch.cuda.Event()
-        done.record(main)
-        copy.wait_event(done)
-        with torch.cuda.stream(copy):
-            h["r"].copy_(d.rewards, non_blocking=True)
-            h["term"].copy_(d.terminated, non_blocking=True)
-            h["trunc"].copy_(d.truncated, non_blocking=True)
-            h["cp"].copy_(d.current_player, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
         # no host wait for the step itself: the next step's kernel reads the next actions from the
-        # pinned buffer in stream order, so the host runs at most one step ahead of the GPU (it
-        # waits for the previous step's results right here)
-        if pending:
-            read(pending.pop())
-        pending.append((batch, ev, h))
+        # pinned buffer in stream order; the host reads the PREVIOUS step's results here (one step
+        # behind), so it runs at most one step ahead of the GPU
+        fetcher.fetch(batch)
         t += 1
 
     def drain():
-        while pending:
-            read(pending.pop())
+        fetcher.drain()
 
     for _ in range(args.warmup):
         one()
@@ -492,8 +469,9 @@ def run_e2e(args, game, dev, world, slot0, B):
             "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": (4 * P + 2 + 4 + 8) * B, "steps": args.steps,
             "path": "public core.batch_step; the DEVICE random policy (fused sampler) writes the next actions into "
                     "pinned host memory and the step kernel reads them from there (zero-copy over PCIe; "
-                    "BBK_ZERO_COPY=0 copies instead); rewards/flags/player D2H on a copy stream, read by the "
-                    "host one step later; the mask and observation stay on the device; same window as value",
+                    "BBK_ZERO_COPY=0 copies instead); rewards/flags/player D2H on a copy stream (session.ResultFetcher: "
+                    "pinned double buffers, one native bbk_fetch_async call per step), read by the host one "
+                    "step later; the mask and observation stay on the device; same window as value",
             "zero_copy": ZERO_COPY}
 
 

@@ -211,6 +211,13 @@ int bbk_check_actions(const uint8_t* mask, const uint8_t* terminated, const uint
 int bbk_count_finished(const uint8_t* terminated, const uint8_t* truncated, int64_t n,
                        unsigned long long* count, void* stream);
 
+/* The host read of a step's results (bench.py:121-129 reads rewards / flags every step): after the
+ * work queued on `main_stream`, `count` (<= 8) device -> host copies dst[i] <- src[i] (bytes[i])
+ * on `copy_stream`, then `done` recorded on it. `after` and `done` are cudaEvent_t handles the
+ * caller owns. One call instead of an event record, a stream wait, per-buffer copies and a record. */
+int bbk_fetch_async(int count, void* const* dst, const void* const* src, const int64_t* bytes,
+                    void* main_stream, void* copy_stream, void* after, void* done);
+
 int bbk_abi_version(void);
 const char* bbk_build_info(void);
 

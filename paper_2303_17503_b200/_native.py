@@ -94,6 +94,7 @@ def _declare(L):
 
     sig("bbk_abi_version", restype=C.c_int)
     sig("bbk_build_info", restype=C.c_char_p)
+    sig("bbk_fetch_async", [C.c_int, P, P, P, P, P, P, P])
     sig("bbk_debug_checks", restype=C.c_int)
     sig("bbk_debug_failures", [C.c_int, P, C.c_int], C.c_int)
     sig("bbk_go_pat_stride", [C.c_int])
@@ -175,11 +176,17 @@ def ptr(t) -> int | None:
 
 def stream_handle(device=None) -> int:
     """cudaStream_t of torch's current stream on `device`, made the CUDA runtime's current device too:
-    every launch goes through here, and a kernel must run on the device that owns its buffers."""
+    every launch goes through here, and a kernel must run on the device that owns its buffers.
+    (torch's raw-stream query: no Python Stream object per launch -- the public step path's host cost.)"""
     import torch
 
+    C_ = torch._C
     if device is not None:
         idx = device.index if isinstance(device, torch.device) else int(device)
-        if idx is not None and torch.cuda.current_device() != idx:
+        if idx is not None and C_._cuda_getDevice() != idx:
             torch.cuda.set_device(idx)
-    return torch.cuda.current_stream(device).cuda_stream
+    else:
+        idx = None
+    if idx is None:
+        idx = C_._cuda_getDevice()
+    return C_._cuda_getCurrentRawStream(idx)

@@ -172,6 +172,18 @@ int bbk_latch_finished(const uint8_t* term, const uint8_t* trunc, const float* r
     return (int)cudaGetLastError();
 }
 
+int bbk_fetch_async(int count, void* const* dst, const void* const* src, const int64_t* bytes,
+                    void* main_stream, void* copy_stream, void* after, void* done) {
+    if (count < 0 || count > 8) return (int)cudaErrorInvalidValue;
+    cudaStream_t ms = (cudaStream_t)main_stream, cs = (cudaStream_t)copy_stream;
+    cudaError_t e = cudaEventRecord((cudaEvent_t)after, ms);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, (cudaEvent_t)after, 0);
+    for (int i = 0; i < count && e == cudaSuccess; i++)
+        if (bytes[i] > 0) e = cudaMemcpyAsync(dst[i], src[i], (size_t)bytes[i], cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && done) e = cudaEventRecord((cudaEvent_t)done, cs);
+    return (int)e;
+}
+
 int bbk_abi_version(void) { return BBK_ABI_VERSION; }
 
 const char* bbk_build_info(void) {

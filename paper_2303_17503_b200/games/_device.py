@@ -187,7 +187,7 @@ class DeviceKernel:
         stream when one is pooled (see _recycle), else freshly allocated."""
         torch = _torch()
         v = DeviceV(self, n, slot0, device, t, limit)
-        stream = torch.cuda.current_stream(device).cuda_stream if torch.device(device).type == "cuda" else 0
+        stream = nat.stream_handle(device) if torch.device(device).type == "cuda" else 0
         pkey = (n, device, obs, stream)
         with _POOLS_LOCK:
             pool = self.__dict__.setdefault("_pools", {}).setdefault(pkey, [])

@@ -19,6 +19,64 @@ from .core import Batch, EngineError, batch_init, batch_step, resolve
 from .rng import RngKey
 
 
+class ResultFetcher:
+    """The per-step host read of a batch's results -- rewards, terminated, truncated and
+    current_player, what the reference's bench loop consumes every step (bench.py:121-129) --
+    without stalling the device: double-buffered pinned host buffers filled on a copy stream by one
+    native call (bbk_fetch_async: event record, stream wait, the copies, a done event) after the
+    step's launch. ``fetch(batch)`` queues batch's copies and returns the PREVIOUS batch's results as
+    numpy arrays (None on the first call), so the host runs one step behind the GPU; ``drain()``
+    returns the last one."""
+
+    FIELDS = ("rewards", "terminated", "truncated", "current_player")
+
+    def __init__(self, n: int, num_players: int, device=None):
+        import ctypes
+
+        import torch
+
+        from . import _native as nat
+
+        self._torch, self._nat, self._C = torch, nat, ctypes
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        shapes = {"rewards": ((n, num_players), torch.float32), "terminated": ((n,), torch.bool),
+                  "truncated": ((n,), torch.bool), "current_player": ((n,), torch.int32)}
+        self.host = [{f: torch.empty(shp, dtype=dt, pin_memory=True) for f, (shp, dt) in shapes.items()}
+                     for _ in range(2)]
+        self._dst = [(ctypes.c_void_p * 4)(*[h[f].data_ptr() for f in self.FIELDS]) for h in self.host]
+        self._bytes = (ctypes.c_int64 * 4)(*[self.host[0][f].numel() * self.host[0][f].element_size()
+                                             for f in self.FIELDS])
+        self.copy = torch.cuda.Stream(self.device)
+        self.after = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        for ev in self.after + self.done:   # materialise the CUDA events (handles for the native call)
+            ev.record(self.copy)
+        self._t = 0
+        self._pending = None
+
+    def _read(self, slot: int) -> dict:
+        self.done[slot].synchronize()
+        return {f: self.host[slot][f].numpy() for f in self.FIELDS}
+
+    def fetch(self, batch):
+        nat = self._nat
+        d = batch.device
+        slot = self._t & 1
+        src = (self._C.c_void_p * 4)(*[getattr(d, f).data_ptr() for f in self.FIELDS])
+        nat.check(nat.lib().bbk_fetch_async(4, self._dst[slot], src, self._bytes, nat.stream_handle(self.device),
+                                            self.copy.cuda_stream, self.after[slot].cuda_event,
+                                            self.done[slot].cuda_event), "bbk_fetch_async")
+        # batch stays referenced until its copies are waited for: its buffers must not be recycled
+        # (stream-ordered reuse covers the main stream only, not the copy stream)
+        prev, self._pending = self._pending, (slot, batch)
+        self._t += 1
+        return None if prev is None else self._read(prev[0])
+
+    def drain(self):
+        prev, self._pending = self._pending, None
+        return None if prev is None else self._read(prev[0])
+
+
 class BatchSession:
     """A batched environment driven from one root seed (bench.py:54-83)."""
 

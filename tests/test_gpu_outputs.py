@@ -57,3 +57,28 @@ def test_pinned_host_actions_zero_copy(game):
         assert np.array_equal(acts[(t + 1) % 2].numpy(), random_actions_device(ref, root.child(2 * t + 3)).cpu().numpy())
         for k in ("legal_action_mask", "rewards", "terminated", "truncated", "current_player", "observation"):
             assert np.array_equal(getattr(zc, k), getattr(ref, k)), (t, k)
+
+
+@pytest.mark.parametrize("game", ["go_19x19", "backgammon", "chess", "tic_tac_toe"])
+def test_result_fetcher_one_step_behind(game):
+    """session.ResultFetcher (bbk_fetch_async): fetch(batch_t) returns batch_{t-1}'s rewards / flags /
+    current player, drain() the last batch's -- equal to the batches' own columns."""
+    import torch
+
+    B = 64
+    sess = bb.BatchSession(game, B, 7, validate=False)
+    spec = bb.core.resolve(game).spec
+    f = bb.ResultFetcher(B, spec.num_players, torch.device("cuda", 0))
+    prev = None
+    assert f.fetch(sess.batch) is None
+    prev = sess.batch
+    for t in range(12):
+        sess.step(sess.sample_random_actions())
+        got = f.fetch(sess.batch)
+        for name in bb.ResultFetcher.FIELDS:
+            np.testing.assert_array_equal(got[name], np.asarray(getattr(prev, name)), err_msg=f"{game} {name} t={t}")
+        prev = sess.batch
+    last = f.drain()
+    for name in bb.ResultFetcher.FIELDS:
+        np.testing.assert_array_equal(last[name], np.asarray(getattr(prev, name)))
+    assert f.drain() is None
