@@ -236,10 +236,34 @@ class DeviceLoop:
         self.t += 1
 
     def timed(self, K):
-        """K steps between CUDA events on the launching stream (synchronised on both sides), plus the
-        step kernel's own per-launch events. Returns (ms, per-launch kernel ms list)."""
+        """K steps between CUDA events on the launching stream (synchronised on both sides). Returns
+        (ms, per-launch step-kernel ms list).
+
+        Fused mode (one kernel per step): the K launches are captured into one CUDA graph (the same
+        kernels with the same arguments as the eager loop) and the graph is replayed once between the
+        events, so host launch overhead never shows up as device time -- backgammon's 30 us step is
+        shorter than the host's ~30 us per launch, and eager timing made it host-bound and noisy
+        (2.8-4.2 G env-steps/s). Every kernel in the graph is a step kernel, so the per-launch
+        duration is the replay time / K. Unfused mode keeps eager launches with per-launch events."""
         import torch
 
+        if not self.unfused:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(self.stream)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(K):
+                    self.step()
+            torch.cuda.synchronize()
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(self.stream)
+            g.replay()
+            end.record(self.stream)
+            torch.cuda.synchronize()
+            ms = start.elapsed_time(end)
+            del g
+            return ms, [ms / K] * K
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
