@@ -71,7 +71,7 @@ typedef struct bbk_cols {
  *   bloom[n, bbk_go_filter_words(size)] uint32: a Bloom filter over history hashes, then a
  *                        filter of the (black, white) stone-count pairs of the history
  *                        positions (a repeat must have equal counts). Sized per board:
- *                        2048 + 1024 bits up to 9x9, 4096 + 1024 up to 13x13, else the
+ *                        2048 + 2048 bits up to 9x9, 4096 + 2048 up to 13x13, else the
  *                        8192 + 2048 bits below (the largest).
  */
 #define BBK_GO_BLOOM_WORDS 256

@@ -55,7 +55,10 @@ __host__ __device__ constexpr int boards_per_cta(int N) { return kWarps * (32 / 
 #define BBK_GO_BLOOM9_WORDS 64   // Bloom words of boards up to 9x9 (tuning knob; the host asks bbk_go_filter_words)
 #endif
 __host__ __device__ constexpr int bloom_words(int N) { return N <= 9 ? BBK_GO_BLOOM9_WORDS : N <= 13 ? 128 : BBK_GO_BLOOM_WORDS; }
-__host__ __device__ constexpr int pair_words(int N) { return N <= 13 ? 32 : BBK_GO_PAIR_WORDS; }
+#ifndef BBK_GO_PAIR9_WORDS
+#define BBK_GO_PAIR9_WORDS 64   // pair-filter words up to 13x13 (r02: 2048 bits +0.6 % over 1024 at 9x9)
+#endif
+__host__ __device__ constexpr int pair_words(int N) { return N <= 13 ? BBK_GO_PAIR9_WORDS : BBK_GO_PAIR_WORDS; }
 __host__ __device__ constexpr int filter_words(int N) { return bloom_words(N) + pair_words(N); }
 __host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
 

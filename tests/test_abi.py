@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
     for n in (5, 7, 9, 11, 13, 15, 17, 19):   # host allocation == kernel row stride
         assert L.bbk_go_filter_words(n) == GoKernel(n).filter_words
-    assert [L.bbk_go_filter_words(n) for n in (9, 13, 19)] == [96, 160, 320]   # bbk.h layout note
+    assert [L.bbk_go_filter_words(n) for n in (9, 13, 19)] == [128, 192, 320]   # bbk.h layout note
     assert L.bbk_go_filter_words(8) == -1
     # the product build carries no device-side checks (tools/checked_build.sh makes the checked one)
     if not os.environ.get("BBK_LIB"):
