@@ -807,7 +807,7 @@ __global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, co
 }
 
 #ifndef BBK_CHESS_GRID_BOARDS
-#define BBK_CHESS_GRID_BOARDS 4   // boards per warp per launch (common.cuh step_grid); 0: persistent grid (r02: 4 = +6 %, 3 = +6.1 %, 8 = +3 %)
+#define BBK_CHESS_GRID_BOARDS 3   // boards per warp per launch (common.cuh step_grid); 0: persistent grid (r02: 3 = +6.3 %, 4 = +6 %, 6 = +4 %, 8 = +3 %)
 #endif
 static int launch(const Params& p, cudaStream_t s) {
     const int64_t need = (p.n + kWarps - 1) / kWarps;
