@@ -1211,12 +1211,13 @@ static int launch_step(const StepParams& p, cudaStream_t stream) {
     }
     const int per_sm = per_sm_dev[dev];
     int64_t need = (p.n + boards_per_cta(N) - 1) / boards_per_cta(N);
-    // Grid: boards up to 13x13 use a persistent grid (the resident CTAs loop over all boards); the
-    // large boards launch about one CTA per 3 boards per warp segment, so CTAs retire and new ones start in
-    // board order. The observation stream then leaves the SMs in a tighter address window: a warp
-    // writing whole records absorbs 7.2 TB/s when each warp writes one record and exits vs 6.2 TB/s
-    // from a persistent grid (tools/write_pattern.cu); go_19x19 +11.5 % early game, +4 % over a full
-    // episode cycle, +1 % late game (r02 A/B, 2-6 boards per warp within 1 %). 9x9 lost 3.7 %.
+    // Grid: whole waves of resident CTAs (wave_grid, common.cuh). The large boards launch about one
+    // CTA per 3 boards per warp segment, so CTAs retire and new ones start in board order and the
+    // observation stream leaves the SMs in a tighter address window: a warp writing whole records
+    // absorbs 7.2 TB/s when each warp writes one record and exits vs 6.2 TB/s from a persistent grid
+    // (tools/write_pattern.cu); go_19x19 +11.5 % early game, +4 % over a full episode cycle. Small
+    // boards (prefetch-sensitive, ALU-bound) run two waves of 8 boards per segment (+0.4 % over a
+    // persistent grid; more CTAs lost up to 3.7 %).
     constexpr int kGridBoards = BBK_GO_GRID_BOARDS >= 0 ? BBK_GO_GRID_BOARDS : (N > 13 ? 3 : 8);   // 19x19 at 7 CTAs: 3 > 4 > 2; 9x9: 8 (two waves) +0.4 % over persistent, 4: -0.8 %
     const int64_t grid = wave_grid((int64_t)num_sms() * per_sm, need, kGridBoards);
     step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(p);
