@@ -33,7 +33,7 @@
 
 namespace go {
 #ifndef BBK_GO_OBS_UNROLL
-#define BBK_GO_OBS_UNROLL 2
+#define BBK_GO_OBS_UNROLL 1   // r02 graph-timed: 1 = +1 % over a 19x19 cycle (2: baseline, 4: -4 %)
 #endif
 constexpr int kGoObsUnroll = BBK_GO_OBS_UNROLL;   // observation chunk loop unroll (tuning knob)
 using namespace bbk;
@@ -725,7 +725,7 @@ __device__ __forceinline__ void init_block(BlockSmem<N>& B) {
 }
 
 #ifndef BBK_GO_NB_UNROLL
-#define BBK_GO_NB_UNROLL 4
+#define BBK_GO_NB_UNROLL 1   // large boards too (r02 graph-timed: +0.5 % 19x19 cycle)
 #endif
 // the placement's neighbour loop: rolled up for the small boards (smaller hot code, +0.7 % at 9x9)
 constexpr int kNbUnroll = BBK_GO_NB_UNROLL;
