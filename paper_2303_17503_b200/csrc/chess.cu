@@ -25,6 +25,13 @@ namespace chess {
 #define BBK_CHESS_PASS_UNROLL 1   // r02: rolled up +2 % (i-cache: 23 % of chess stalls are no-instruction)
 #endif
 constexpr int kChessPassUnroll = BBK_CHESS_PASS_UNROLL;   // the observation pattern's two square passes
+#ifndef BBK_CHESS_OR_UNROLL
+#define BBK_CHESS_OR_UNROLL 4
+#endif
+#ifndef BBK_CHESS_PAST_UNROLL
+#define BBK_CHESS_PAST_UNROLL 1   // r02: rolled +2.8 % (2: +1.7 %, 4: +0.3 %)
+#endif
+constexpr int kChessOrUnroll = BBK_CHESS_OR_UNROLL, kChessPastUnroll = BBK_CHESS_PAST_UNROLL;
 #ifndef BBK_CHESS_OBS_UNROLL
 #define BBK_CHESS_OBS_UNROLL 2   // r02 (with the pass loop rolled): 2 = +1.9 % over 4, 1 = 0
 #endif
@@ -691,7 +698,7 @@ __global__ void __launch_bounds__(kWarps * 32, BBK_CHESS_MIN_CTAS) step_kernel(P
             const int sabs = v ^ fl;
             // 119-bit pattern of square v (bit k = plane k) in two registers
             uint64_t plo = clo, phi = chi;
-#pragma unroll
+#pragma unroll kChessPastUnroll
             for (int t = 0; t < 8; t++) {
                 const uint8_t pc = S.past[t][sabs];
                 const int base = 14 * t;
@@ -704,7 +711,7 @@ __global__ void __launch_bounds__(kWarps * 32, BBK_CHESS_MIN_CTAS) step_kernel(P
             const uint32_t w[4] = {(uint32_t)plo, (uint32_t)(plo >> 32), (uint32_t)phi, (uint32_t)(phi >> 32)};
             // OR the 119-bit pattern into the stream at bit offset 119 v
             const int off = 119 * v, wi = off >> 5, sh = off & 31;
-#pragma unroll
+#pragma unroll kChessOrUnroll
             for (int j = 0; j < 4; j++) {
                 uint32_t lo = w[j] << sh;
                 uint32_t hi = sh ? (w[j] >> (32 - sh)) : 0u;
