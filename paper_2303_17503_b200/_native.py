@@ -181,6 +181,12 @@ def stream_handle(device=None) -> int:
     import torch
 
     C_ = torch._C
+    if not hasattr(C_, "_cuda_getCurrentRawStream"):   # older / newer torch: the public (slower) path
+        if device is not None:
+            idx = device.index if isinstance(device, torch.device) else int(device)
+            if idx is not None and torch.cuda.current_device() != idx:
+                torch.cuda.set_device(idx)
+        return torch.cuda.current_stream(device).cuda_stream
     if device is not None:
         idx = device.index if isinstance(device, torch.device) else int(device)
         if idx is not None and C_._cuda_getDevice() != idx:
