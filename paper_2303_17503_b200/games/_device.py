@@ -62,7 +62,16 @@ class Lineage:
     predecessor's history prefix is then still intact, so any of them can be
     branched (the trail is kept in full). Once a batch step runs, resets may have
     rewritten a slot's history, and only the last ``keep`` predecessors stay
-    branchable (the games' depth limits); anything older raises StaleBatch.
+    branchable in the shared store (the games' depth limits).
+
+    A batch that falls off the trail while the caller still holds it is not lost:
+    ``mark_batch_step`` / ``advance`` / ``drop`` return the uids they removed, and
+    the kernel gives each batch still alive (``track`` keeps weak references) a
+    private copy of the store BEFORE the next launch can overwrite its history
+    (DeviceKernel.release). Every state therefore stays steppable at any depth, as
+    reference states are (core.py:1-7); the copy is paid only by batches that are
+    held, never by a loop that drops its predecessors. StaleBatch remains only for a
+    uid the lineage never saw.
     """
 
     def __init__(self, uid: int, t: int = 0, append_only: bool = True):
@@ -70,6 +79,12 @@ class Lineage:
         self.head_t = t
         self.trail: list[int] = []
         self.append_only = append_only
+        self.refs: dict[int, weakref.ref] = {}
+
+    def track(self, v) -> "Lineage":
+        """Remember batch v weakly (see release)."""
+        self.refs[v.uid] = weakref.ref(v)
+        return self
 
     def depth(self, uid: int) -> int:
         if uid == self.head:
@@ -79,12 +94,21 @@ class Lineage:
         except ValueError:
             return 1 << 30
 
-    def mark_batch_step(self, keep: int = 2) -> None:
-        if self.append_only:
-            self.append_only = False
-            self.trail = self.trail[:keep]
+    def _removed(self, before: list[int]) -> list[int]:
+        now = set(self.trail)
+        now.add(self.head)
+        return [u for u in before if u not in now]
 
-    def advance(self, parent: int, child: int, keep: int = 2, child_t: int | None = None) -> None:
+    def mark_batch_step(self, keep: int = 2) -> list[int]:
+        if not self.append_only:
+            return []
+        before = list(self.trail)
+        self.append_only = False
+        self.trail = self.trail[:keep]
+        return self._removed(before)
+
+    def advance(self, parent: int, child: int, keep: int = 2, child_t: int | None = None) -> list[int]:
+        before = [self.head] + self.trail
         lim = None if self.append_only else keep
         if parent == self.head:
             self.trail = ([parent] + self.trail)[:lim]
@@ -94,6 +118,14 @@ class Lineage:
         self.head = child
         if child_t is not None:
             self.head_t = child_t
+        return self._removed(before)
+
+    def drop(self, uids) -> list[int]:
+        """Take uids off the trail (a game whose store wraps, chess.RingKernel.window)."""
+        gone = set(uids)
+        before = list(self.trail)
+        self.trail = [u for u in self.trail if u not in gone]
+        return self._removed(before)
 
 
 class DeviceV:
@@ -342,7 +374,8 @@ class DeviceKernel:
         if validate:
             self.validate(v, a)
         if v.store is not None and not scalar:
-            v.store.lineage.mark_batch_step(self.branch_keep)
+            lin = v.store.lineage
+            self.release(lin, lin.mark_batch_step(self.branch_keep))
         sk = self._slot_keys(slot_keys, v.device)
         ks = 0 if key is None else key_state(key)
         if out is None:
@@ -367,11 +400,50 @@ class DeviceKernel:
         out.store = v.store
 
     # ------------------------------------------------ branching (shared per-env stores)
-    branch_keep = 2   # predecessors a batch-stepped lineage keeps branchable
+    branch_keep = 2   # predecessors a batch-stepped lineage keeps branchable in the shared store
+    window = None     # steps a trail entry of an append-only lineage stays intact (None: unbounded)
+    snapshots = 0     # batches given a private store by release (a count for the tests)
+
+    def advance_lineage(self, lin: Lineage, v: DeviceV, out: DeviceV) -> None:
+        """out (stepped from v) becomes lin's head; live batches that fall off the trail get a
+        private store before out's launch (release)."""
+        gone = lin.advance(v.uid, out.uid, self.branch_keep, out.t)
+        lin.track(out)
+        if self.window is not None and lin.append_only:
+            old = []
+            for u in lin.trail:
+                r = lin.refs.get(u)
+                w = None if r is None else r()
+                if w is None or w.uid != u or out.t - w.t > self.window:
+                    old.append(u)
+            if old:
+                gone += lin.drop(old)
+        self.release(lin, gone)
+
+    def release(self, lin: Lineage, uids: list) -> None:
+        """Batches that left lin's trail: each one still alive gets a private copy of the store
+        now, while its history is intact (the trail invariant) and before the next launch can
+        overwrite it, and becomes the head of its own lineage. So every state the caller holds
+        stays steppable (reference value semantics, core.py:1-7) at the price of one store copy
+        per held batch; a loop that drops its predecessors never pays it."""
+        for u in uids:
+            r = lin.refs.pop(u, None)
+            w = None if r is None else r()
+            if w is None or w.uid != u or w.store is None or w.store.lineage is not lin:
+                continue
+            store = w.store.clone_rows()
+            store.lineage = Lineage(w.uid, w.t).track(w)
+            w.store = store
+            self.private_store_ready(w)
+            self.snapshots += 1
+
+    def private_store_ready(self, w: DeviceV) -> None:
+        """Game hook: make a copied store consistent with w (Go: filters and chain labels)."""
 
     def branch_depth(self, v: DeviceV) -> int:
-        """How far v is behind the head of its store's lineage (0 = head); raises StaleBatch when
-        the shared store may no longer hold v's history."""
+        """How far v is behind the head of its store's lineage (0 = head). StaleBatch only for a
+        batch its lineage cannot account for (release keeps every live batch on a trail or in a
+        store of its own)."""
         from ..core import StaleBatch
 
         if v.store is None or v.store.lineage is None:
@@ -381,8 +453,8 @@ class DeviceKernel:
         if d == 0:
             return 0
         if d >= (1 << 30) or (d > self.branch_keep and not lin.append_only):
-            raise StaleBatch(f"{self.game_id}: batch is too far behind its trajectory (only the newest batch and "
-                             f"its last {self.branch_keep} predecessors remain steppable after a batch step)")
+            raise StaleBatch(f"{self.game_id}: batch is not on its trajectory's trail (its history store may "
+                             "have been overwritten)")
         self.check_branch(v, lin)
         return d
 

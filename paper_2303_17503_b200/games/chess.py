@@ -72,6 +72,9 @@ class RingStore:
         return RingStore(torch.empty((n,) + tuple(self.hist.shape[1:]), dtype=self.hist.dtype,
                                      device=self.hist.device))
 
+    def clone_rows(self, rows=slice(None)) -> "RingStore":
+        return RingStore(self.hist[rows].clone())
+
 
 class ChessCoreView:
     __slots__ = ("board", "role_to_move", "castling", "ep", "halfmove", "rep", "terminal", "rewards", "mask")
@@ -113,7 +116,7 @@ class RingKernel(DeviceKernel):
 
     def launch_init(self, v, ks, sk):
         v.store = self.alloc_store(v)
-        v.store.lineage = Lineage(v.uid)
+        v.store.lineage = Lineage(v.uid).track(v)
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_init")
         nat.check(fn(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                      nat.stream_handle(v.device)), f"bbk_{self.prefix}_init")
@@ -148,7 +151,7 @@ class RingKernel(DeviceKernel):
             raise ValueError(f"{self.game_id}: positions must be {self.board_bytes} + {self.misc_bytes} bytes")
         v = self.new_v(n, slot0, device, 0, limit, obs)
         v.store = self.alloc_store(v)
-        v.store.lineage = Lineage(v.uid)
+        v.store.lineage = Lineage(v.uid).track(v)
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_load")
         nat.check(fn(self.cols(v), self.state_struct(v), nat.ptr(boards), nat.ptr(misc), n, slot0,
                      0 if key is None else key_state(key), None, limit, nat.stream_handle(device)),
@@ -165,7 +168,7 @@ class RingKernel(DeviceKernel):
             store = RingStore(store.hist.clone())
             store.lineage = Lineage(v.uid, v.t, old.append_only)
         out.store = store
-        store.lineage.advance(v.uid, out.uid, self.branch_keep, out.t)
+        self.advance_lineage(store.lineage, v, out)
 
     def launch_step(self, v, out, a, ks, sk, limit):
         fn = getattr(nat.lib(), f"bbk_{self.prefix}_step")
@@ -194,7 +197,7 @@ class RingKernel(DeviceKernel):
     def slice_store(self, v, w, i):
         self.branch_depth(v)   # StaleBatch if stepping v's descendants overwrote its history
         w.store = RingStore(v.store.hist[i:i + 1].clone())
-        w.store.lineage = Lineage(w.uid, w.t)
+        w.store.lineage = Lineage(w.uid, w.t).track(w)
 
 
 class ChessKernel(RingKernel):
@@ -208,6 +211,12 @@ class ChessKernel(RingKernel):
 
     def parse_position(self, text):
         return parse_fen(text)
+
+    # A trail entry t of an append-only (scalar) lineage reads plies [t + 1 - M, t] of the ring,
+    # M <= 101 (a live state's half-move clock is below 100), so it is intact while the head is
+    # fewer than 128 - 101 + 1 = 28 plies ahead; older entries still held get their own ring
+    # first (DeviceKernel.advance_lineage / release), with two plies of margin.
+    window = 25
 
     def check_branch(self, v, lin):
         """The 128-ply ring is reused modulo 128: stepping v reads plies [t + 1 - M, t] (M = the

@@ -168,12 +168,15 @@ class GoKernel(DeviceKernel):
 
     def launch_init(self, v: DeviceV, ks: int, sk) -> None:
         v.store = self.new_store(v.n, v.limit, v.device)
-        v.store.lineage = Lineage(v.uid)
+        v.store.lineage = Lineage(v.uid).track(v)
         cols, st, store = self.out_cols(v), self.state_struct(v), v.store.struct()
         nat.check(nat.lib().bbk_go_init(self.size, cols, st, store, v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                         nat.stream_handle(v.device)), "bbk_go_init")
 
     branch_keep = 2   # a live slot's history prefix survives two batch steps (see history_of)
+
+    def private_store_ready(self, w: DeviceV) -> None:
+        self.rebuild_filters(w)
 
     def rebuild_filters(self, w: DeviceV) -> None:
         """Recompute w's store from w's own state after a branch copied a store that later steps may
@@ -197,7 +200,7 @@ class GoKernel(DeviceKernel):
             store.lineage = Lineage(v.uid, v.t, old.append_only)
             self.rebuild_filters(_with_store(v, store))
         out.store = store
-        store.lineage.advance(v.uid, out.uid, self.branch_keep, out.t)
+        self.advance_lineage(store.lineage, v, out)
 
     def launch_step(self, v, out, a, ks, sk, limit) -> None:
         nat.check(nat.lib().bbk_go_step(self.size, self.komi, int(self.allow_self_capture), self.cols(v), self.state_struct(v), self.out_cols(out),
@@ -224,14 +227,15 @@ class GoKernel(DeviceKernel):
         depth = self.branch_depth(v)
         s = v.store
         w.store = s.clone_rows(slice(i, i + 1))
-        w.store.lineage = Lineage(w.uid, w.t)
+        w.store.lineage = Lineage(w.uid, w.t).track(w)
         if depth > 0:
             self.rebuild_filters(w)
 
     def history_of(self, v: DeviceV, i: int, hist_len: int) -> frozenset:
-        """Slot i's superko set: entries [0, hist_len) of the shared append-only store. A live slot's
-        prefix survives while the batch is at most two steps behind the lineage head (a reset
-        rewrites entry 0 with the same value 0, the next placement entry 1)."""
+        """Slot i's superko set: entries [0, hist_len) of v's history store. A live slot's prefix
+        survives in the shared store while the batch is at most two steps behind the lineage head (a
+        reset rewrites entry 0 with the same value 0, the next placement entry 1); a held batch
+        that falls further behind gets a store of its own first (DeviceKernel.release)."""
         self.branch_depth(v)   # raises StaleBatch when the store may no longer hold v's prefix
         row = v.store.history[i, :hist_len].cpu().numpy().view(np.uint64)
         return frozenset(int(x) for x in row)

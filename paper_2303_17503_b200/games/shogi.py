@@ -106,7 +106,7 @@ class ShogiKernel(RingKernel):
 
     def launch_init(self, v, ks, sk):
         v.store = self.alloc_store(v)
-        v.store.lineage = Lineage(v.uid)
+        v.store.lineage = Lineage(v.uid).track(v)
         nat.check(nat.lib().bbk_shogi_init(self.out_cols(v), self.state_struct(v), v.n, v.slot0, ks, nat.ptr(sk), v.limit,
                                            nat.stream_handle(v.device)), "bbk_shogi_init")
 

@@ -183,7 +183,7 @@ def search(v, rows, key_states, simulations: int = 32, *, exploration: float = m
     keys = torch.as_tensor(np.asarray([int(k) & ((1 << 64) - 1) for k in key_states], dtype=np.uint64)
                            .view(np.int64)).to(dev)
     # roots: v rows -> staging a -> pool rows s * M; untried sets from the staging masks
-    depth = kern.branch_depth(v)   # StaleBatch when v's shared history store has moved on
+    depth = kern.branch_depth(v)   # > 0: v branches off a shared store that its descendants moved on
     copy_rows(kern.row_tensors(v), kern.row_tensors(p.sa), rows_t, None, n, stream)
     if depth > 0 and hasattr(kern, "rebuild_filters"):
         kern.rebuild_filters(p.sa)   # the store rows may carry entries of v's descendants

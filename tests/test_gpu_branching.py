@@ -5,8 +5,9 @@ log), plus the host-side thread-safety of the shared kernel objects.
 * scalar trajectories (core.init / core.step) never auto-reset, so their stores are append-only:
   ANY earlier state can be stepped again (the reference's mcts_agent re-steps stored node states),
   and the original trajectory stays steppable afterwards;
-* batch trajectories keep the newest batch and its last predecessors steppable (Go two, chess /
-  shogi one) and raise StaleBatch beyond, never a silently wrong state;
+* batch trajectories share the store with the newest batch and its last predecessors (Go two,
+  chess / shogi one); a held batch that falls further behind gets a private store first, so it
+  stays steppable too (DeviceKernel.release), and a loop that drops its batches never pays that;
 * search() and slicing honour the same rule.
 """
 
@@ -17,7 +18,6 @@ import pytest
 
 import paper_2303_17503_b200 as bb
 from paper_2303_17503_b200.agents import random_actions
-from paper_2303_17503_b200.core import StaleBatch
 
 pytestmark = pytest.mark.gpu
 
@@ -66,27 +66,69 @@ def test_scalar_states_branch_at_any_depth(game):
 
 
 @pytest.mark.parametrize("game,keep", [("go_9x9", 2), ("go_19x19", 2), ("chess", 1), ("shogi", 1)])
-def test_batch_lineage_branch_limits(game, keep):
+def test_batch_states_branch_at_any_depth(game, keep):
+    """Every held batch stays steppable: within keep of the head it branches off the shared store;
+    a held batch that falls further behind was given a store of its own before its history could
+    be overwritten (DeviceKernel.release). Each branch equals a from-scratch replay."""
     root = bb.RngKey(3)
+    kern = bb.core.resolve(game).batch_kernel
     b = [bb.batch_init(game, root.child(0), 64)]
-    for t in range(1, 6):
+    s0 = kern.snapshots
+    T = 12
+    for t in range(1, T + 1):
         b.append(bb.batch_step(b[-1], random_actions(b[-1], root.child(2 * t - 1)), root.child(2 * t)))
-    # depth <= keep: branching works and equals a from-scratch replay; the old head stays steppable
-    d = keep
-    src = b[-1 - d]
-    acts = random_actions(src, root.child(777))
-    got = bb.batch_step(src, acts, root.child(778))
-    r = bb.batch_init(game, root.child(0), 64)
-    for t in range(1, 6 - d):
-        r = bb.batch_step(r, random_actions(r, root.child(2 * t - 1)), root.child(2 * t))
-    want = bb.batch_step(r, acts, root.child(778))
-    assert bb.batch_fingerprint(got) == bb.batch_fingerprint(want)
-    assert np.array_equal(got.observation, want.observation)
+    assert kern.snapshots - s0 == T - keep   # every held batch older than keep was copied once
+    for d in (keep, keep + 1, T // 2, T):
+        src = b[-1 - d]
+        acts = random_actions(src, root.child(777 + d))
+        got = bb.batch_step(src, acts, root.child(778))
+        r = bb.batch_init(game, root.child(0), 64)
+        for t in range(1, T + 1 - d):
+            r = bb.batch_step(r, random_actions(r, root.child(2 * t - 1)), root.child(2 * t))
+        want = bb.batch_step(r, acts, root.child(778))
+        assert bb.batch_fingerprint(got) == bb.batch_fingerprint(want), (game, d)
+        assert np.array_equal(got.observation, want.observation)
+    # the head's trajectory is untouched by all of that and steps on like a fresh replay
     nxt = bb.batch_step(b[-1], random_actions(b[-1], root.child(11)), root.child(12))
-    assert nxt.size == 64
-    # deeper than keep: StaleBatch (never a silently wrong state)
-    with pytest.raises(StaleBatch):
-        bb.batch_step(b[-2 - keep], random_actions(b[-2 - keep], root.child(5)), root.child(6))
+    r = bb.batch_init(game, root.child(0), 64)
+    for t in range(1, T + 1):
+        r = bb.batch_step(r, random_actions(r, root.child(2 * t - 1)), root.child(2 * t))
+    assert bb.batch_fingerprint(nxt) == bb.batch_fingerprint(
+        bb.batch_step(r, random_actions(r, root.child(11)), root.child(12)))
+
+
+@pytest.mark.parametrize("game", ["go_19x19", "chess", "shogi"])
+def test_a_loop_that_drops_its_batches_copies_no_store(game):
+    """The copy is paid only by held batches: the reference's step loop (and the result fetcher that
+    keeps the previous batch until its copies land) never triggers one."""
+    root = bb.RngKey(5)
+    kern = bb.core.resolve(game).batch_kernel
+    b = bb.batch_init(game, root.child(0), 256)
+    fetch = bb.ResultFetcher(256, 2)
+    s0 = kern.snapshots
+    for t in range(1, 40):
+        b = bb.batch_step(b, random_actions(b, root.child(2 * t - 1)), root.child(2 * t))
+        fetch.fetch(b)
+    fetch.drain()
+    assert kern.snapshots == s0
+
+
+def test_scalar_chess_states_older_than_the_ring_window_stay_steppable():
+    """A scalar chess trajectory keeps its states on one 128-ply ring; states the caller holds get
+    their own ring before the head is far enough ahead to overwrite their window."""
+    key = bb.RngKey(8)
+    states, acts = _walk("chess", key, 70)
+    assert len(states) > 60
+    for j in (2, 20):
+        s = states[j]
+        a = int(np.flatnonzero(s.legal_action_mask)[-1])
+        got = bb.step(s, a, key.child(5000 + j))
+        r = bb.init("chess", key.child(0))
+        for t, x in enumerate(acts[:j], start=1):
+            r = bb.step(r, x, key.child(2 * t + 1))
+        want = bb.step(r, a, key.child(5000 + j))
+        assert bb.state_fingerprint(got) == bb.state_fingerprint(want), j
+        assert np.array_equal(bb.observe(got, 0), bb.observe(want, 0))
 
 
 def test_search_on_a_predecessor_batch_equals_search_before_stepping():
@@ -104,8 +146,8 @@ def test_search_on_a_predecessor_batch_equals_search_before_stepping():
     after = np.asarray(mcts_actions(b, root.child(100), 8))   # b is two steps behind now
     assert np.array_equal(before, after)
     bb.batch_step(b2, random_actions(b2, root.child(105)), root.child(106))
-    with pytest.raises(StaleBatch):
-        mcts_actions(b, root.child(100), 8)
+    later = np.asarray(mcts_actions(b, root.child(100), 8))   # three behind: b has its own store
+    assert np.array_equal(before, later)
 
 
 def test_threads_stepping_the_same_game_match_a_sequential_run():

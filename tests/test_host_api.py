@@ -70,6 +70,63 @@ def test_lineage_allows_head_and_recent_branches():
     assert lin.depth(4) == 0 and lin.depth(2) == 1 and lin.depth(3) > 2
 
 
+def test_lineage_reports_what_falls_off_the_trail():
+    lin = Lineage(1)
+    assert lin.advance(1, 2) == [] and lin.advance(2, 3) == [] and lin.advance(3, 4) == []
+    assert lin.trail == [3, 2, 1]                     # append-only: the full trail
+    assert lin.mark_batch_step(2) == [1]              # a batch step keeps two predecessors
+    assert lin.mark_batch_step(2) == []
+    assert lin.advance(4, 5) == [2] and lin.trail == [4, 3]
+    assert lin.advance(4, 6) == [5] and lin.trail == [4, 3]   # branch in place: the old head goes
+    assert lin.drop([4]) == [4] and lin.trail == [3]
+
+
+def test_release_gives_held_batches_their_own_store():
+    """DeviceKernel.release: a live batch that leaves the trail gets a private store copy and its
+    own lineage; dead batches and batches reusing a uid slot (the bench's ping-pong) are skipped."""
+    import gc
+
+    from paper_2303_17503_b200.games._device import DeviceKernel
+
+    class Store:
+        def __init__(self, rows):
+            self.rows, self.lineage = rows, None
+
+        def clone_rows(self):
+            return Store(list(self.rows))
+
+    class B:
+        def __init__(self, uid, t, store):
+            self.uid, self.t, self.store = uid, t, store
+
+    class K(DeviceKernel):
+        ready = []
+
+        def private_store_ready(self, w):
+            self.ready.append(w.uid)
+
+    k = K()
+    shared = Store([7, 8])
+    shared.lineage = lin = Lineage(1)
+    held = [B(1, 0, shared)]
+    lin.track(held[0])
+    for u in range(2, 6):
+        b = B(u, u - 1, shared)
+        lin.advance(u - 1, u, 2, u - 1)
+        lin.track(b)
+        held.append(b)
+    lin.mark_batch_step(2)
+    gone = lin.advance(5, 6, 2, 5)
+    held[2].uid = 99                                  # object reused under another uid: not this batch
+    del held[1]
+    gc.collect()
+    k.release(lin, [1, 2, 3] + gone)
+    b1 = held[0]
+    assert b1.store is not shared and b1.store.rows == [7, 8] and b1.store.lineage.head == 1
+    assert b1.store.lineage.depth(1) == 0 and k.ready == [1] and k.snapshots == 1
+    assert held[1].store is shared                    # the reused object keeps the shared store
+
+
 def test_session_key_schedule_matches_reference_formula():
     # bench.py:54-83: init root.child(0), actions before step t root.child(2t-1), step t root.child(2t)
     root = bb.RngKey(0)
