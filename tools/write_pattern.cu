@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/wp tools/write_pattern.cu && /tmp/wp
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 // one warp per record (records of `rec` floats, flat stream, 16-B chunks of the aligned interior)
@@ -153,6 +154,47 @@ __global__ void rec_nonpersist_strided(float* out, int64_t n, int rec) {
     }
 }
 
+// (e) bulk (TMA-engine) stores: each warp fills a CHUNK-byte shared-memory buffer (double
+// buffered) and one lane hands it to cp.async.bulk.global.shared::cta; K boards per warp strided
+// by the grid's warp count. The record's unaligned head/tail floats go out as plain stores.
+template <int CHUNK, int K>
+__global__ void rec_bulk(float* out, int64_t n, int rec) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float* buf0 = reinterpret_cast<float*>(sm + wid * 2 * CHUNK);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + wid;
+    int par = 0;
+    for (int k = 0; k < K; k++) {
+        const int64_t b = w + k * nw;
+        if (b >= n) break;
+        const int64_t F0 = b * rec;
+        const int head = (int)((4 - (F0 & 3)) & 3);
+        const float v = (float)(b & 1);
+        const int body = ((rec - head) >> 2) << 2;
+        const int tail = rec - head - body;
+        if (lane < head) out[F0 + lane] = v;
+        if (lane < tail) out[F0 + head + body + lane] = v;
+        float* g = out + F0 + head;
+        for (int off = 0; off < body; off += CHUNK / 4) {
+            const int cnt = min(CHUNK / 4, body - off);
+            float* buf = buf0 + par * (CHUNK / 4);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            for (int j = lane * 4; j < cnt; j += 128) *reinterpret_cast<float4*>(buf + j) = make_float4(v, v, v, v);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                             :: "l"(g + off), "r"((unsigned)__cvta_generic_to_shared(buf)), "r"(cnt * 4) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            par ^= 1;
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     const int64_t n = 131072;
     const int rec = 19 * 19 * 17;
@@ -174,6 +216,23 @@ int main() {
         ms /= K;
         printf("%-40s %.3f ms  %.0f GB/s\n", name, ms, bytes / (ms * 1e6));
     };
+    if (getenv("WP_BULK")) {
+        timeit("per record 256, 1/warp (n/4 CTAs)", [&] { per_record256<<<(unsigned)(n / 4), 128>>>(out, n, rec); });
+        timeit("per record 256, 3 strided/warp", [&] { rec_nonpersist_strided<3><<<(unsigned)((n + 11) / 12), 128>>>(out, n, rec); });
+        cudaFuncSetAttribute(rec_bulk<4096, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        cudaFuncSetAttribute(rec_bulk<4096, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        cudaFuncSetAttribute(rec_bulk<8192, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        timeit("bulk 2K chunks, 1/warp", [&] { rec_bulk<2048, 1><<<(unsigned)(n / 4), 128, 4 * 2 * 2048>>>(out, n, rec); });
+        timeit("bulk 2K chunks, 3 strided/warp", [&] { rec_bulk<2048, 3><<<(unsigned)((n + 11) / 12), 128, 4 * 2 * 2048>>>(out, n, rec); });
+        timeit("bulk 4K chunks, 1/warp", [&] { rec_bulk<4096, 1><<<(unsigned)(n / 4), 128, 4 * 2 * 4096>>>(out, n, rec); });
+        timeit("bulk 4K chunks, 3 strided/warp", [&] { rec_bulk<4096, 3><<<(unsigned)((n + 11) / 12), 128, 4 * 2 * 4096>>>(out, n, rec); });
+        timeit("bulk 8K chunks, 3 strided/warp", [&] { rec_bulk<8192, 3><<<(unsigned)((n + 11) / 12), 128, 4 * 2 * 8192>>>(out, n, rec); });
+        timeit("bulk 1K chunks, 3 strided/warp", [&] { rec_bulk<1024, 3><<<(unsigned)((n + 11) / 12), 128, 4 * 2 * 1024>>>(out, n, rec); });
+        timeit("flat 256 (again)", [&] { flat256<<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
+        cudaError_t e = cudaDeviceSynchronize();
+        printf("%s\n", cudaGetErrorString(e));
+        return 0;
+    }
     timeit("flat grid-stride (148x8 x 256)", [&] { flat<<<148 * 8, 256>>>((float4*)out, (int64_t)(bytes / 16)); });
     timeit("flat 256-bit stores", [&] { flat256<<<148 * 8, 256>>>(out, (int64_t)(bytes / 32)); });
     timeit("flat unroll 4", [&] { flat_unroll4<<<148 * 8, 256>>>((float4*)out, (int64_t)(bytes / 16)); });
