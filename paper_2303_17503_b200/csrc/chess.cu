@@ -118,6 +118,7 @@ struct Params {
     int force_reset;
     const uint8_t* load_board;   // kLoad: positions to start from, [n, 64] / [n, 8] (stm, castle, ep, half-move)
     const uint8_t* load_misc;
+    int64_t tail_ctas;   // one-pass CTAs at the end of the grid (common.cuh pass_map)
 };
 
 __device__ __forceinline__ bool on(int r, int f) { return (unsigned)r < 8u && (unsigned)f < 8u; }
@@ -441,20 +442,21 @@ __global__ void __launch_bounds__(kWarps * 32, BBK_CHESS_MIN_CTAS) step_kernel(P
     __syncthreads();
     WarpSmem& S = sm[threadIdx.x >> 5];
     const int lane = lane_id();
-    const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+    const PassMap pm = pass_map(p.n, kWarps, p.tail_ctas, threadIdx.x >> 5);
+    const int64_t nwarps = pm.stride, bend = pm.end;
     unsigned long long eps = 0;
-    const int64_t b0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const int64_t b0 = pm.b0;
     uint64_t cur = 0ull;   // this board's scalar fields (lane j holds field j)
     bool pf_ready = false;
     const FieldRef fref = field_ref(p, lane_id());
-    for (int64_t b = b0; b < p.n; b += nwarps) {
+    for (int64_t b = b0; b < bend; b += nwarps) {
         if (!p.force_reset && !pf_ready) {   // first board of the warp: fetch synchronously
             cur = load_field(fref, b);
             issue_prefetch(S, p, b, cur, lane);
         }
         // the next board's scalars are in flight while this board is processed
         const int64_t nb = b + nwarps;
-        const uint64_t nxt = (!p.force_reset && nb < p.n) ? load_field(fref, nb) : 0ull;
+        const uint64_t nxt = (!p.force_reset && nb < bend) ? load_field(fref, nb) : 0ull;
         const uint32_t f_term = __shfl_sync(BBK_FULL, (uint32_t)cur, 0) | (__shfl_sync(BBK_FULL, (uint32_t)cur, 5) << 8);
         const bool reset = p.force_reset || (f_term & 0xFFFFu) != 0u;
         if (!p.force_reset) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(kWarps * 32, BBK_CHESS_MIN_CTAS) step_kernel(P
         const int rep = reps > 2 ? 2 : reps;
         __syncwarp();   // the prefetch area (board, past boards, ring meta) is free now: issue the next board's state
         pf_ready = false;
-        if (!p.force_reset && nb < p.n) {
+        if (!p.force_reset && nb < bend) {
             issue_prefetch(S, p, nb, nxt, lane);
             cur = nxt;
             pf_ready = true;
@@ -824,13 +826,21 @@ __global__ void observe_kernel(bbk_chess_state st, const int32_t* step_count, co
 #ifndef BBK_CHESS_GRID_BOARDS
 #define BBK_CHESS_GRID_BOARDS 3   // boards per warp per launch (common.cuh step_grid); 0: persistent grid (r02: 3 = +6.3 %, 4 = +6 %, 6 = +4 %, 8 = +3 %)
 #endif
-static int launch(const Params& p, cudaStream_t s) {
+#ifndef BBK_CHESS_TAIL_PCT
+#define BBK_CHESS_TAIL_PCT 150   // one-pass CTAs at the end of the grid, % of the resident CTAs (r02: +2.3 %; 100: +1.6 %)
+#endif
+template <bool kLoad>
+static void launch_grid(const Params& p, cudaStream_t s) {
     const int64_t need = (p.n + kWarps - 1) / kWarps;
-    if (p.load_board) {
-        step_kernel<true><<<(unsigned)step_grid(step_kernel<true>, kWarps * 32, 0, need, BBK_CHESS_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
-    } else {
-        step_kernel<false><<<(unsigned)step_grid(step_kernel<false>, kWarps * 32, 0, need, BBK_CHESS_GRID_BOARDS), kWarps * 32, 0, s>>>(p);
-    }
+    const int64_t resident = resident_ctas(step_kernel<kLoad>, kWarps * 32, 0);
+    const int64_t grid = wave_grid(resident, need, BBK_CHESS_GRID_BOARDS);
+    Params q = p;
+    q.tail_ctas = tail_ctas(grid, resident, BBK_CHESS_TAIL_PCT);
+    step_kernel<kLoad><<<(unsigned)grid, kWarps * 32, 0, s>>>(q);
+}
+static int launch(const Params& p, cudaStream_t s) {
+    if (p.load_board) launch_grid<true>(p, s);
+    else launch_grid<false>(p, s);
     return (int)cudaGetLastError();
 }
 

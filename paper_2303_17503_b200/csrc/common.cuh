@@ -101,12 +101,48 @@ inline int64_t wave_grid(int64_t resident, int64_t need, int boards_per_warp) {
     return g < need ? g : need;
 }
 template <class Kernel>
-inline int64_t step_grid(Kernel kernel, int threads, size_t smem, int64_t need, int boards_per_warp) {
+inline int64_t resident_ctas(Kernel kernel, int threads, size_t smem) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-    return wave_grid((int64_t)sms * (per_sm < 1 ? 1 : per_sm), need, boards_per_warp);
+    return (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+}
+template <class Kernel>
+inline int64_t step_grid(Kernel kernel, int threads, size_t smem, int64_t need, int boards_per_warp) {
+    return wave_grid(resident_ctas(kernel, threads, smem), need, boards_per_warp);
+}
+
+// Tail of one-pass CTAs (pass_map): `pct` % of the resident CTAs, for a grid of several waves.
+inline int64_t tail_ctas(int64_t grid, int64_t resident, int pct) {
+    if (grid <= resident || pct <= 0) return 0;
+    const int64_t t = resident * pct / 100;
+    return t < grid / 2 ? t : grid / 2;
+}
+
+// Board mapping of a step grid (a pass = one board per warp or warp segment, `per_cta` boards per
+// CTA): the first gridDim.x - tail CTAs grid-stride over every pass but the last `tail` ones,
+// which the last `tail` CTAs take one each. Those launch last, so the grid drains with short CTAs
+// filling the slots the long ones free instead of idling behind the slowest multi-pass CTA
+// (r02: go_9x9 +3.2 %, go_19x19 +0.8 %). tail = 0: the plain grid stride.
+struct PassMap {
+    int64_t b0, stride, end;
+};
+__device__ __forceinline__ PassMap pass_map(int64_t n, int per_cta, int64_t tail, int slot) {
+    const int64_t passes = (n + per_cta - 1) / per_cta;
+    const int64_t front = (int64_t)gridDim.x - tail;
+    PassMap m;
+    if ((int64_t)blockIdx.x >= front) {
+        m.b0 = (passes - tail + ((int64_t)blockIdx.x - front)) * per_cta + slot;
+        m.stride = n > 0 ? n : 1;
+        m.end = n;
+    } else {
+        const int64_t e = (passes - tail) * per_cta;
+        m.b0 = (int64_t)blockIdx.x * per_cta + slot;
+        m.stride = front * per_cta;
+        m.end = e < n ? e : n;
+    }
+    return m;
 }
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {

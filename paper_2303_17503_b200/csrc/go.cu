@@ -235,6 +235,7 @@ struct StepParams {
     double komi;
     int force_reset;
     int self_capture;   // make_game(allow_self_capture=True) (go.py:155-173, 249-255)
+    int64_t tail_ctas;  // CTAs at the end of the grid that take one pass each (see step_kernel)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -733,6 +734,10 @@ constexpr int kNbUnroll = BBK_GO_NB_UNROLL;
 #ifndef BBK_GO_GRID_BOARDS
 #define BBK_GO_GRID_BOARDS -1   // boards per warp segment per launch: 0 persistent, -1 per-size default
 #endif
+#ifndef BBK_GO_TAIL_PCT
+#define BBK_GO_TAIL_PCT 150     // one-pass CTAs at the end of a multi-wave grid, % of the resident CTAs (r02: go_19x19 +0.8 %, go_9x9 +3.2 %; 50: -8 % at 9x9, 300: = 150)
+#endif
+constexpr int kGoTailPct = BBK_GO_TAIL_PCT;
 // resident CTAs per SM the register budget is sized for: small boards fit 8 (shared memory allows it)
 #ifndef BBK_GO_CTAS_SMALL
 #define BBK_GO_CTAS_SMALL 8
@@ -756,25 +761,26 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
     const int sl = g.sl;
     WarpSmem<N>& S = B.w[threadIdx.x / L];
     const uint32_t rowm = sl < N ? ROW : 0u;
-    const int64_t nboards = (int64_t)gridDim.x * boards_per_cta(N);   // boards in flight (grid stride)
+    const PassMap pm = pass_map(p.n, boards_per_cta(N), p.tail_ctas, threadIdx.x / L);   // common.cuh
+    const int64_t nboards = pm.stride, bend = pm.end;
     unsigned long long eps = 0;
     // next-board prefetch: scalar columns in registers (lane j holds field j), `pat` via
     // cp.async into an idle tail of the scratch union (not touched by mask/obs emission)
     uint16_t* pat_pf = reinterpret_cast<uint16_t*>(S.capx);   // dead from the mask on (see WarpSmem)
     uint16_t* lab_pf = pat_pf + PS;
     uint16_t* lab = reinterpret_cast<uint16_t*>(S.u.uf.bl);   // this board's chain labels
-    const int64_t b0 = (int64_t)blockIdx.x * boards_per_cta(N) + threadIdx.x / L;
+    const int64_t b0 = pm.b0;
     const FieldRefWide fref = widen(field_ref(p, sl), p.in.terminated);
     uint32_t pf_sh = 0u;
     uint64_t pf_raw = 0ull;
-    if (!p.force_reset && b0 < p.n) {
+    if (!p.force_reset && b0 < bend) {
         if constexpr (kDeferFields<N>) pf_raw = load_field_raw(fref, b0, pf_sh);
         else pf_raw = load_field(fref, b0);
     }
     bool pat_ready = false;
 
-    for (int64_t b = b0; b < p.n; b += nboards) {
-        if (!p.force_reset && b + nboards < p.n && sl < (4 * filter_words(N) + 127) / 128) {
+    for (int64_t b = b0; b < bend; b += nboards) {
+        if (!p.force_reset && b + nboards < bend && sl < (4 * filter_words(N) + 127) / 128) {
             // warm L2 with the next board's Bloom filter (cp.async'd mid-board)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(
                 reinterpret_cast<const char*>(p.store.bloom + (b + nboards) * (int64_t)filter_words(N)) + 128 * sl));
@@ -1034,7 +1040,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_ctas(N)) step_kernel(StepPara
         }
         g.sync();   // staged mask bytes are overwritten by the observation pattern next
         pat_ready = false;
-        if (!p.force_reset && b + nboards < p.n) {   // issue the next board's loads now
+        if (!p.force_reset && b + nboards < bend) {   // issue the next board's loads now
             const int64_t nb = b + nboards;
             if constexpr (kDeferFields<N>) pf_raw = load_field_raw(fref, nb, pf_sh);
             else pf_raw = load_field(fref, nb);
@@ -1219,8 +1225,11 @@ static int launch_step(const StepParams& p, cudaStream_t stream) {
     // boards (prefetch-sensitive, ALU-bound) run two waves of 8 boards per segment (+0.4 % over a
     // persistent grid; more CTAs lost up to 3.7 %).
     constexpr int kGridBoards = BBK_GO_GRID_BOARDS >= 0 ? BBK_GO_GRID_BOARDS : (N > 13 ? 3 : 8);   // 19x19 at 7 CTAs: 3 > 4 > 2; 9x9: 8 (two waves) +0.4 % over persistent, 4: -0.8 %
-    const int64_t grid = wave_grid((int64_t)num_sms() * per_sm, need, kGridBoards);
-    step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(p);
+    const int64_t resident = (int64_t)num_sms() * per_sm;
+    const int64_t grid = wave_grid(resident, need, kGridBoards);
+    StepParams q = p;
+    q.tail_ctas = tail_ctas(grid, resident, kGoTailPct);
+    step_kernel<N><<<(unsigned)grid, kWarps * 32, smem, stream>>>(q);
     return (int)cudaGetLastError();
 }
 

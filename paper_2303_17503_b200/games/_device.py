@@ -36,7 +36,7 @@ def _torch():
 
 _UID = [0]
 _UID_LOCK = threading.Lock()
-_POOLS_LOCK = threading.Lock()
+_POOLS_LOCK = threading.RLock()   # re-entrant: a finalizer (_recycle) may run inside a locked region (GC)
 # per-thread fused outputs of the launch being built (the kernel objects are shared per game)
 _TLS = threading.local()
 

@@ -46,7 +46,7 @@ def test_reference_suite_through_the_device_plugin():
         env["BBK_LIB"] = os.path.join(ROOT, env["BBK_LIB"]) if not os.path.isabs(env["BBK_LIB"]) else env["BBK_LIB"]
     cmd = [sys.executable, "-m", "pytest", "-p", "paper_2303_17503_b200.reference_plugin", "-p", "no:cacheprovider",
            "-q", "-rA", "--rootdir", TESTS] + [os.path.join(TESTS, s) for s in SELECTION]
-    r = subprocess.run(cmd, cwd=TESTS, env=env, capture_output=True, text=True, timeout=1500)
+    r = subprocess.run(cmd, cwd=TESTS, env=env, capture_output=True, text=True, timeout=900)
     log_dir = os.path.join(ROOT, "gpurun_out")
     os.makedirs(log_dir, exist_ok=True)
     with open(os.path.join(log_dir, "reference_hookin.log"), "w") as fh:
